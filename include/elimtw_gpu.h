@@ -1,0 +1,99 @@
+/* Additive C ABI of the B200 build (libelimtw.so.1). Nothing here changes
+ * elimtw.h; these entry points expose the device seam the reference keeps
+ * internal, so tests and tools can drive it with plain pointers.
+ *
+ * Vertex sets cross the ABI as two little-endian u64 words (bits 0..127);
+ * adjacency is `rows[2*v + w]`. Statuses and error buffers follow elimtw.h.
+ *
+ *   etwg_decide        replaces decide()        proj/src/dp.hpp:78-79
+ *   etwg_expand_layer  replaces expand_layer()  proj/src/dp.hpp:68-70
+ *   etwg_solve_layers  solve() with the DpConfig::observer seam
+ *                      (dp.hpp:31-32) capturing every search-phase layer
+ *   etwg_bloom_insert  one device insert_and_check batch (bloom.cpp:86-97)
+ *   etwg_max_clique / etwg_split / etwg_disjoint_paths / etwg_improve_graph /
+ *   etwg_mmw_lower_bound   host preprocessing (preprocess.hpp:23-46,
+ *                      mmw.hpp:46-47) for parity tests without a GPU
+ */
+#ifndef ELIMTW_GPU_H
+#define ELIMTW_GPU_H
+
+#include "elimtw.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct etwg_run etwg_run;
+
+/* 1 when a CUDA device is usable; fills name/SM count when non-NULL. */
+ELIMTW_API int etwg_device_info(int* device, int* sm_count, char* name, size_t name_len);
+
+/* One decision run tw(g) <= k? on the device. dedup: etw_dedup. rounds < 0
+ * selects n-k-1. keep_layers copies every layer back (test seam). */
+ELIMTW_API etw_status etwg_decide(int n, const uint64_t* rows, int k, const uint64_t* forbidden,
+                                  int dedup, int use_mmw, uint64_t max_layer_states,
+                                  int bloom_bits_per_element, int bloom_hashes, int rounds,
+                                  int keep_layers, etwg_run** out, char* err, size_t err_len);
+
+/* One round over an explicit input layer (sets: 2 words per state). */
+ELIMTW_API etw_status etwg_expand_layer(int n, const uint64_t* rows, int k,
+                                        const uint64_t* forbidden, const uint64_t* sets,
+                                        const uint32_t* hist, size_t count, int dedup,
+                                        int use_mmw, uint64_t max_layer_states,
+                                        int bloom_bits_per_element, int bloom_hashes,
+                                        etwg_run** out, char* err, size_t err_len);
+
+/* Full etw_solve capturing every layer of the search phase in call order. */
+ELIMTW_API etw_status etwg_solve_layers(const etw_graph* g, const etw_options* opts,
+                                        etwg_run** out, char* err, size_t err_len);
+
+/* 0 feasible, 1 infeasible, 2 indeterminate */
+ELIMTW_API int etwg_run_outcome(const etwg_run* r);
+ELIMTW_API int etwg_run_overflowed(const etwg_run* r);
+ELIMTW_API void etwg_run_witness(const etwg_run* r, uint64_t* set2, uint32_t* hist);
+ELIMTW_API int etwg_run_round_count(const etwg_run* r);
+/* 6 u64 per round: k, round, expanded, emitted, duplicates, mmw_pruned */
+ELIMTW_API void etwg_run_rounds(const etwg_run* r, uint64_t* stats, uint8_t* overflowed);
+ELIMTW_API int etwg_run_layer_count(const etwg_run* r);
+ELIMTW_API uint64_t etwg_run_layer_size(const etwg_run* r, int i);
+/* k and round of captured layer i (etwg_solve_layers) */
+ELIMTW_API void etwg_run_layer_tag(const etwg_run* r, int i, int* k, int* round);
+ELIMTW_API void etwg_run_layer(const etwg_run* r, int i, uint64_t* sets2, uint32_t* hist);
+ELIMTW_API void etwg_run_free(etwg_run* r);
+
+/* Device Bloom filter sized for `expected` elements; inserts `count` keys
+ * (words u64 each) concurrently, one per thread, and reports each key's
+ * novelty plus the final bit array (m/8 bytes into bits_out when non-NULL).
+ * Returns m, 0 on error. */
+ELIMTW_API uint64_t etwg_bloom_insert(uint64_t expected, int bits_per_element, int hashes,
+                                      const uint64_t* keys, int words, size_t count,
+                                      uint8_t* novel_out, uint32_t* bits_out, size_t bits_words);
+
+/* Profiling counters of the device engine (milliseconds / bytes / counts):
+ * out[0..] = decide_ms, expand_ms, insert_ms, append_ms, clear_ms, fused_ms,
+ * expand_launches, insert_launches, append_launches, clear_launches,
+ * fused_launches, kernel_launches, layer_bytes, dedup_bytes, expanded,
+ * h2d_bytes, d2h_bytes. Returns the number of values written. */
+ELIMTW_API int etwg_times(double* out, int len);
+/* CUDA events on the engine stream around a region; end synchronizes and
+ * returns the device milliseconds in between. */
+ELIMTW_API void etwg_timer_begin(void);
+ELIMTW_API double etwg_timer_end(void);
+ELIMTW_API void etwg_set_profiling(int on);
+ELIMTW_API void etwg_reset_times(void);
+
+/* host preprocessing (no GPU needed); rows as above */
+ELIMTW_API void etwg_graph_rows(const etw_graph* g, uint64_t* rows);
+ELIMTW_API void etwg_max_clique(int n, const uint64_t* rows, uint64_t* out2);
+ELIMTW_API void etwg_disjoint_paths(int n, const uint64_t* rows, uint8_t* out);
+ELIMTW_API void etwg_improve_graph(int n, const uint64_t* rows, int k, uint64_t* out_rows);
+ELIMTW_API int etwg_mmw_lower_bound(int n, const uint64_t* rows, const uint64_t* s, int cap);
+/* verts: concatenated original ids; returns block count */
+ELIMTW_API int etwg_split(int n, const uint64_t* rows, int mode, int* verts, int* sizes,
+                          int* cuts);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ELIMTW_GPU_H */
