@@ -76,7 +76,7 @@ struct Control {
 
 struct Params {
     int n, k, rounds, free_count;
-    int hashes, bpe, any_pop, pad;
+    int hashes, bpe, any_pop, flags;  // flags: ETWG_DEBUG bits (tests only)
     u64 max_states;
     u64 forbidden[2];
     u64 rows[kMaxVertices][2];
@@ -547,13 +547,13 @@ __global__ void __launch_bounds__(kThreads) k_exact_insert(const Params* __restr
 
 template <int W>
 __device__ __forceinline__ bool bloom_insert(unsigned* bits, unsigned* locks, u64 m, int hashes,
-                                             const Set<W>& key) {
+                                             const Set<W>& key, bool single_lock = false) {
     const unsigned h1 = murmur_key<W>(key, kSeed1);
     const unsigned h2 = murmur_key<W>(key, kSeed2);
     // probe i at (h1 + i*h2) mod m, i = 1..hashes, stepped incrementally
     const u64 step = static_cast<u64>(h2) % m;
     u64 pos = (static_cast<u64>(h1) + static_cast<u64>(h2)) % m;
-    unsigned* lock = locks + (h1 % kStripes);
+    unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
     while (atomicCAS(lock, 0u, 1u) != 0u) __nanosleep(64);
     __threadfence();
     bool novel = false;
@@ -575,8 +575,9 @@ __global__ void __launch_bounds__(kThreads) k_bloom_clear(const Params* __restri
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
     const u64 m = bloom_bits_for(round_cap(*P, E), P->bpe);
-    const u64 words = m / 32;
+    u64 words = m / 32;
     const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+    if (P->flags & 4) words = B.bloom_cap;
     if (words > B.bloom_cap) {
         if (gtid == 0) {
             C->need = words;
@@ -631,8 +632,8 @@ __global__ void __launch_bounds__(kThreads) k_bloom_insert(const Params* __restr
                 // emission rank) inserts; the others are duplicates outright
                 unsigned group = __match_any_sync(act, key.w[0]);
                 if constexpr (W == 2) group &= __match_any_sync(act, key.w[1]);
-                const bool leader = (__ffs(group) - 1) == lane;
-                if (leader && bloom_insert<W>(B.bloom, B.locks, m, P->hashes, key))
+                const bool leader = (P->flags & 1) ? true : (__ffs(group) - 1) == lane;
+                if (leader && bloom_insert<W>(B.bloom, (P->flags & 2) ? B.locks + 0 : B.locks, m, P->hashes, key, (P->flags & 2) != 0))
                     atomicOr(&novel_words[wslot + src][v >> 5], 1u << (v & 31));
             }
         }
@@ -1009,6 +1010,7 @@ private:
     Control* h_ctl_ = nullptr;
     Bufs b_{};
     u64 table_dirty_bytes_ = 0;  // table bytes possibly holding keys of an earlier decide
+    int table_layout_ = 0;       // slot layout (W) the clean part of the table is in
     int grid_ = 0;
     cudaEvent_t ev_[2] = {nullptr, nullptr};
     cudaEvent_t tev_[2] = {nullptr, nullptr};
@@ -1067,6 +1069,7 @@ private:
         p.hashes = cfg.bloom_hashes;
         p.bpe = cfg.bloom_bits_per_element;
         p.any_pop = any_pop;
+        if (const char* dbg = std::getenv("ETWG_DEBUG")) p.flags = std::atoi(dbg);
         p.max_states = cfg.max_layer_states;
         p.forbidden[0] = forbidden.w[0];
         p.forbidden[1] = forbidden.w[1];
@@ -1125,6 +1128,7 @@ private:
         check(cudaMalloc(&b_.table, cap * 32), "table");
         b_.table_cap = cap;
         table_dirty_bytes_ = cap * 32;  // fresh memory: reset everything before use
+        table_layout_ = 0;
     }
 
     void ensure_bloom(u64 words) {
@@ -1135,8 +1139,14 @@ private:
         b_.bloom_cap = cap;
     }
 
+    // The "empty" pattern differs between the 16-byte (W=1) and 32-byte
+    // (W=2) slot layouts, so switching layouts re-initialises the whole table.
     void reset_table(int W) {
         ensure_table(u64{1} << 20);
+        if (W != table_layout_) {
+            table_dirty_bytes_ = b_.table_cap * 32;
+            table_layout_ = W;
+        }
         if (table_dirty_bytes_ == 0) return;
         const u64 slot_bytes = W == 1 ? 16 : 32;
         u64 slots = std::min((table_dirty_bytes_ + slot_bytes - 1) / slot_bytes,
@@ -1201,7 +1211,8 @@ private:
         ensure_bloom(u64{1} << 22);
         if (!prof.on) check(cudaEventRecord(ev_[0], stream_), "event");
         auto t0 = std::chrono::steady_clock::now();
-        int chunk = observer ? 1 : 4;
+        const bool sync_each = (h_params_->flags & 8) != 0;
+        int chunk = observer || sync_each ? 1 : 4;
         for (;;) {
             const int start = static_cast<int>(h_ctl_->round);
             const int end = std::min(rounds, start + chunk);
@@ -1223,7 +1234,7 @@ private:
                 }
             }
             if (c.stop || static_cast<int>(c.round) >= rounds) break;
-            chunk = std::min(chunk * 2, 32);
+            if (!observer && !sync_each) chunk = std::min(chunk * 2, 32);  // observer: one round per check
         }
         if (cfg.dedup == DedupMode::exact_set) {
             const u64 slot_bytes = W == 1 ? 16 : 32;
