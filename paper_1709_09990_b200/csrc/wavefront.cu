@@ -551,8 +551,34 @@ __device__ __forceinline__ bool bloom_insert(unsigned* bits, unsigned* locks, u6
     const unsigned h1 = murmur_key<W>(key, kSeed1);
     const unsigned h2 = murmur_key<W>(key, kSeed2);
     // probe i at (h1 + i*h2) mod m, i = 1..hashes, stepped incrementally
-    const u64 step = static_cast<u64>(h2) % m;
-    u64 pos = (static_cast<u64>(h1) + static_cast<u64>(h2)) % m;
+    // (h1 + h2) mod m and h2 mod m; 32-bit division whenever m fits
+    u64 step, first;
+    if (m <= 0xFFFFFFFFull) {
+        const unsigned m32 = static_cast<unsigned>(m);
+        const unsigned s = h2 % m32;
+        const u64 f = static_cast<u64>(h1 % m32) + s;
+        step = s;
+        first = f >= m ? f - m : f;
+    } else {
+        step = static_cast<u64>(h2) % m;
+        first = (static_cast<u64>(h1) + static_cast<u64>(h2)) % m;
+    }
+    // Fast path without the lock: when every probe bit is already set the
+    // key is a duplicate in any serialisation of the concurrent inserts
+    // (most children are: dups outnumber novel states ~6:1), so only inserts
+    // that can still be novel pay for the stripe lock and the atomics.
+    {
+        u64 pos = first;
+        bool all_set = true;
+        for (int i = 1; i <= hashes; ++i) {
+            const unsigned word = __ldcg(bits + (pos >> 5));
+            all_set &= ((word >> (pos & 31)) & 1u) != 0;
+            pos += step;
+            if (pos >= m) pos -= m;
+        }
+        if (all_set) return false;
+    }
+    u64 pos = first;
     unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
     while (atomicCAS(lock, 0u, 1u) != 0u) __nanosleep(64);
     __threadfence();
