@@ -4,7 +4,7 @@
 // mmw.cpp:20-146).
 //
 // Per round (one BFS layer of the Held-Karp prefix DP) the device runs:
-//   bloom : k_bloom_clear -> k_expand -> k_bloom_insert -> k_append<mask>
+//   bloom : k_round_bloom (one fused kernel per round)
 //   exact : k_expand -> k_exact_insert -> k_append<probe>
 //
 //   k_expand       one thread per parent S. The components of G[S] are
@@ -49,14 +49,19 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxRounds = 130;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kStripes = 65536;
+// Bloom stripe locks. The reference uses 65,536 mutex stripes keyed by
+// h1 (bloom.cpp:18-23); any key -> stripe map keeps inserts of one key
+// serialised, and ~10^5 concurrent device threads need more stripes to keep
+// unrelated keys from contending.
+constexpr int kStripes = 1 << 20;
 constexpr unsigned kSeed1 = 0x9747B28Cu;  // bloom.hpp:24
 constexpr unsigned kSeed2 = 0x5EEDBA5Eu;  // bloom.hpp:25
 
 using u64 = unsigned long long;
 
 struct RoundStats {
-    u64 expanded, offered, unique, emitted, mmw_pruned, pad;
+    u64 expanded, offered, unique, emitted, mmw_pruned;
+    u64 ticket;  // tile ticket of the round's scan pass
     unsigned overflowed, valid;
 };
 
@@ -68,8 +73,8 @@ struct Control {
     unsigned round;     // next round to run
     unsigned stop;      // 1 once a layer came out empty or all rounds ran
     unsigned abort;     // AbortCode
-    unsigned ticket;    // tile ticket of the append pass
-    unsigned exits;     // CTAs that finished the append pass
+    unsigned epoch;     // look-back tag of the current round attempt (never 0)
+    unsigned exits;     // CTAs that finished the round's last pass
     unsigned pad;
     RoundStats rs[kMaxRounds];
 };
@@ -87,7 +92,7 @@ struct Bufs {
     unsigned* hist[2];
     u64* cmask;
     u64* table;
-    unsigned* bloom;
+    unsigned* bloom[2];  // two filters, alternating by round parity
     unsigned* locks;
     u64* tiles;
     u64 layer_cap;   // states per layer buffer
@@ -367,11 +372,8 @@ __global__ void __launch_bounds__(kThreads) k_expand(const Params* __restrict__ 
     __syncthreads();
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
-    const u64 ntiles = (E + kThreads - 1) / kThreads;
     const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
     const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
-    if (gtid == 0) C->ticket = 0;
-    for (u64 i = gtid; i < ntiles; i += gstride) B.tiles[i] = 0;
 
     const Set<W> forbidden = param_set<W>(P->forbidden);
     const u64* in = B.keys[r & 1];
@@ -545,15 +547,25 @@ __global__ void __launch_bounds__(kThreads) k_exact_insert(const Params* __restr
 // ----------------------------------------------------------------------
 // K2b: Bloom dedup on the reference's bit positions (bloom.cpp:86-97)
 
-template <int W>
-__device__ __forceinline__ bool bloom_insert(unsigned* bits, unsigned* locks, u64 m, int hashes,
-                                             const Set<W>& key, bool single_lock = false) {
-    const unsigned h1 = murmur_key<W>(key, kSeed1);
-    const unsigned h2 = murmur_key<W>(key, kSeed2);
-    // probe i at (h1 + i*h2) mod m, i = 1..hashes, stepped incrementally
-    // (h1 + h2) mod m and h2 mod m; 32-bit division whenever m fits
-    u64 step, first;
-    if (m <= 0xFFFFFFFFull) {
+// Stripe lock with acquire / release semantics (no full fences): the 17
+// relaxed atomicOr of a locked insert stay between the two.
+__device__ __forceinline__ void stripe_lock(unsigned* lock) {
+    unsigned old;
+    for (;;) {
+        asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "l"(lock) : "memory");
+        if (old == 0) return;
+        __nanosleep(64);
+    }
+}
+
+__device__ __forceinline__ void stripe_unlock(unsigned* lock) {
+    asm volatile("st.release.gpu.global.b32 [%0], 0;" ::"l"(lock) : "memory");
+}
+
+// Probe positions (h1 + i*h2) mod m, i = 1..hashes (bloom.cpp:90-91),
+// stepped incrementally: pos_{i+1} = pos_i + (h2 mod m) - [>= m]*m.
+__device__ __forceinline__ void probe_start(unsigned h1, unsigned h2, u64 m, u64& first, u64& step) {
+    if (m <= 0xFFFFFFFFull) {  // 32-bit division whenever m fits
         const unsigned m32 = static_cast<unsigned>(m);
         const unsigned s = h2 % m32;
         const u64 f = static_cast<u64>(h1 % m32) + s;
@@ -563,13 +575,49 @@ __device__ __forceinline__ bool bloom_insert(unsigned* bits, unsigned* locks, u6
         step = static_cast<u64>(h2) % m;
         first = (static_cast<u64>(h1) + static_cast<u64>(h2)) % m;
     }
+}
+
+// insert_and_check (bloom.cpp:86-97) on the device. H > 0 fixes the hash
+// count at compile time so all probe loads / atomics are issued back to
+// back; H == 0 is the generic runtime-count loop.
+template <int W, int H>
+__device__ __forceinline__ bool bloom_insert_h(unsigned* bits, unsigned* locks, u64 m, int hashes,
+                                               const Set<W>& key, bool single_lock) {
+    const unsigned h1 = murmur_key<W>(key, kSeed1);
+    const unsigned h2 = murmur_key<W>(key, kSeed2);
+    u64 first, step;
+    probe_start(h1, h2, m, first, step);
     // Fast path without the lock: when every probe bit is already set the
     // key is a duplicate in any serialisation of the concurrent inserts
-    // (most children are: dups outnumber novel states ~6:1), so only inserts
-    // that can still be novel pay for the stripe lock and the atomics.
-    {
+    // (most children are: duplicates outnumber novel states ~6:1), so only
+    // inserts that can still be novel pay for the stripe lock and atomics.
+    bool all_set = true;
+    if constexpr (H > 0) {  // requires m < 2^32: positions fit 32 bits
+        unsigned pos[H];
+        unsigned word[H];
+        const unsigned m32 = static_cast<unsigned>(m), step32 = static_cast<unsigned>(step);
+        pos[0] = static_cast<unsigned>(first);
+#pragma unroll
+        for (int i = 1; i < H; ++i) {
+            const unsigned p = pos[i - 1] + step32;  // < 2m: wraps past 2^32 only if m > 2^31
+            pos[i] = (p >= m32 || p < pos[i - 1]) ? p - m32 : p;
+        }
+#pragma unroll
+        for (int i = 0; i < H; ++i) word[i] = __ldcg(bits + (pos[i] >> 5));
+#pragma unroll
+        for (int i = 0; i < H; ++i) all_set &= ((word[i] >> (pos[i] & 31)) & 1u) != 0;
+        if (all_set) return false;
+        unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
+        stripe_lock(lock);
+#pragma unroll
+        for (int i = 0; i < H; ++i) word[i] = atomicOr(bits + (pos[i] >> 5), 1u << (pos[i] & 31));
+        stripe_unlock(lock);
+        bool novel = false;
+#pragma unroll
+        for (int i = 0; i < H; ++i) novel |= ((word[i] >> (pos[i] & 31)) & 1u) == 0;
+        return novel;
+    } else {
         u64 pos = first;
-        bool all_set = true;
         for (int i = 1; i <= hashes; ++i) {
             const unsigned word = __ldcg(bits + (pos >> 5));
             all_set &= ((word >> (pos & 31)) & 1u) != 0;
@@ -577,103 +625,28 @@ __device__ __forceinline__ bool bloom_insert(unsigned* bits, unsigned* locks, u6
             if (pos >= m) pos -= m;
         }
         if (all_set) return false;
-    }
-    u64 pos = first;
-    unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
-    while (atomicCAS(lock, 0u, 1u) != 0u) __nanosleep(64);
-    __threadfence();
-    bool novel = false;
-    for (int i = 1; i <= hashes; ++i) {
-        const unsigned bit = 1u << (pos & 31);
-        const unsigned old = atomicOr(bits + (pos >> 5), bit);
-        novel |= (old & bit) == 0;
-        pos += step;
-        if (pos >= m) pos -= m;
-    }
-    __threadfence();
-    atomicExch(lock, 0u);
-    return novel;
-}
-
-__global__ void __launch_bounds__(kThreads) k_bloom_clear(const Params* __restrict__ P,
-                                                          Control* C, Bufs B) {
-    if (halted(C)) return;
-    const unsigned r = C->round;
-    const u64 E = C->count[r & 1];
-    const u64 m = bloom_bits_for(round_cap(*P, E), P->bpe);
-    u64 words = m / 32;
-    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-    if (P->flags & 4) words = B.bloom_cap;
-    if (words > B.bloom_cap) {
-        if (gtid == 0) {
-            C->need = words;
-            C->abort = kGrowBloom;
+        pos = first;
+        unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
+        stripe_lock(lock);
+        bool novel = false;
+        for (int i = 1; i <= hashes; ++i) {
+            const unsigned bit = 1u << (pos & 31);
+            const unsigned old = atomicOr(bits + (pos >> 5), bit);
+            novel |= (old & bit) == 0;
+            pos += step;
+            if (pos >= m) pos -= m;
         }
-        return;
+        stripe_unlock(lock);
+        return novel;
     }
-    const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
-    uint4* w4 = reinterpret_cast<uint4*>(B.bloom);
-    const u64 n4 = words / 4;  // m is a multiple of 64 bits: words is even
-    for (u64 i = gtid; i < n4; i += gstride) w4[i] = make_uint4(0, 0, 0, 0);
-    for (u64 i = n4 * 4 + gtid; i < words; i += gstride) B.bloom[i] = 0;
 }
 
 template <int W>
-__global__ void __launch_bounds__(kThreads) k_bloom_insert(const Params* __restrict__ P,
-                                                           Control* C, Bufs B) {
-    __shared__ unsigned novel_words[kThreads][2 * W];
-    if (halted(C)) return;
-    const unsigned r = C->round;
-    const u64 E = C->count[r & 1];
-    const u64 m = bloom_bits_for(round_cap(*P, E), P->bpe);
-    const int lane = threadIdx.x & 31;
-    const int wslot = threadIdx.x & ~31;
-    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-    const u64 warp = gtid >> 5;
-    const u64 nwarps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
-    const u64* in = B.keys[r & 1];
-    for (u64 base = warp * 32; base < E; base += nwarps * 32) {
-        const u64 idx = base + lane;
-        const bool valid = idx < E;
-        const Set<W> M = valid ? load_set<W>(B.cmask, idx) : Set<W>::zero();
-        const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-#pragma unroll
-        for (int i = 0; i < 2 * W; ++i) novel_words[threadIdx.x][i] = 0;
-        __syncwarp();
-        WarpFlat f;
-        f.scan(M.count());
-        for (int t = 0; t < f.total; t += 32) {
-            const int j = t + lane;
-            const int src = f.source(j);
-            const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
-            const Set<W> Ms = shfl_set<W>(M, src);
-            const Set<W> Ss = shfl_set<W>(S, src);
-            const bool active = j < f.total;
-            const unsigned act = __ballot_sync(kFull, active);
-            if (active) {
-                const int v = nth_member<W>(Ms, j - excl);
-                Set<W> key = Ss;
-                key.add(v);
-                // identical keys inside the warp: only the lowest lane (lowest
-                // emission rank) inserts; the others are duplicates outright
-                unsigned group = __match_any_sync(act, key.w[0]);
-                if constexpr (W == 2) group &= __match_any_sync(act, key.w[1]);
-                const bool leader = (P->flags & 1) ? true : (__ffs(group) - 1) == lane;
-                if (leader && bloom_insert<W>(B.bloom, (P->flags & 2) ? B.locks + 0 : B.locks, m, P->hashes, key, (P->flags & 2) != 0))
-                    atomicOr(&novel_words[wslot + src][v >> 5], 1u << (v & 31));
-            }
-        }
-        __syncwarp();
-        if (valid) {
-            Set<W> nm;
-#pragma unroll
-            for (int i = 0; i < W; ++i)
-                nm.w[i] = novel_words[threadIdx.x][2 * i] |
-                          (static_cast<u64>(novel_words[threadIdx.x][2 * i + 1]) << 32);
-            store_set<W>(B.cmask, idx, nm);
-        }
-        __syncwarp();
-    }
+__device__ __forceinline__ bool bloom_insert(unsigned* bits, unsigned* locks, u64 m, int hashes,
+                                             const Set<W>& key, bool single_lock = false) {
+    return hashes == 17 && m <= 0xFFFFFFFFull
+               ? bloom_insert_h<W, 17>(bits, locks, m, hashes, key, single_lock)
+               : bloom_insert_h<W, 0>(bits, locks, m, hashes, key, single_lock);
 }
 
 template <int W>
@@ -690,33 +663,94 @@ __global__ void k_bloom_batch(const u64* keys, u64 count, unsigned* bits, unsign
 // (replaces the cursor append dp.cpp:96-117 and the rank sort + truncation
 // dp.cpp:150-157)
 
-constexpr u64 kFlagAgg = u64{1} << 62;
-constexpr u64 kFlagPre = u64{2} << 62;
-constexpr u64 kValMask = (u64{1} << 62) - 1;
+// Tile status word: [epoch:24][flag:2][value:38]. The epoch changes with
+// every round attempt, so statuses left by earlier rounds read as "not yet
+// published" and the status array never needs clearing between rounds.
+constexpr u64 kFlagAgg = u64{1} << 38;
+constexpr u64 kFlagPre = u64{2} << 38;
+constexpr u64 kValMask = (u64{1} << 38) - 1;
+constexpr unsigned kEpochMask = (1u << 24) - 1;
 
-__device__ __forceinline__ u64 look_back(u64* tiles, u64 tile, u64 total) {
+__device__ __forceinline__ u64 look_back(u64* tiles, u64 tile, u64 total, unsigned epoch) {
     volatile u64* vt = tiles;
+    const u64 tag = static_cast<u64>(epoch & kEpochMask) << 40;
     if (tile == 0) {
-        vt[0] = kFlagPre | total;
+        vt[0] = tag | kFlagPre | total;
         return 0;
     }
-    vt[tile] = kFlagAgg | total;
+    vt[tile] = tag | kFlagAgg | total;
     u64 prefix = 0;
     u64 t = tile - 1;
     for (;;) {
-        u64 s = vt[t];
-        u64 flag = s & ~kValMask;
-        if (flag == 0) {
+        const u64 s = vt[t];
+        if ((s >> 40) != (tag >> 40) || (s & (kFlagAgg | kFlagPre)) == 0) {
             __nanosleep(20);
             continue;
         }
         prefix += s & kValMask;
-        if (flag == kFlagPre) break;
+        if (s & kFlagPre) break;
         --t;
     }
     __threadfence();
-    vt[tile] = kFlagPre | (prefix + total);
+    vt[tile] = tag | kFlagPre | (prefix + total);
     return prefix;
+}
+
+// Writes the tile's survivors (mask M over parents S with histories H) in
+// rank order: the warp's survivors occupy one contiguous run starting at
+// warp_start, so consecutive lanes store consecutive states.
+template <int W>
+__device__ __forceinline__ void append_survivors(const Set<W>& M, const Set<W>& S, unsigned H,
+                                                 u64 warp_start, u64 limit, u64* out,
+                                                 unsigned* hout) {
+    const int lane = threadIdx.x & 31;
+    WarpFlat f;
+    f.scan(M.count());
+    for (int t = 0; t < f.total; t += 32) {
+        const int j = t + lane;
+        const int src = f.source(j);
+        const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
+        const Set<W> Ms = shfl_set<W>(M, src);
+        const Set<W> Ss = shfl_set<W>(S, src);
+        const unsigned Hs = __shfl_sync(kFull, H, src);
+        const u64 pos = warp_start + j;
+        if (j < f.total && pos < limit) {  // capacity wall: drop the newest (dp.cpp:107,152-155)
+            const int v = nth_member<W>(Ms, j - excl);
+            Set<W> key = Ss;
+            key.add(v);
+            store_set<W>(out, pos, key);
+            hout[pos] = (Hs << 8) | static_cast<unsigned>(v & 0xFF);  // push_history
+        }
+    }
+}
+
+// The last CTA out publishes the round (all CTAs have read the round state
+// by then, so advancing it cannot race with a late starter). Called by every
+// CTA with all threads after its last tile.
+__device__ __forceinline__ void finish_round(const Params* P, Control* C, const Bufs& B, unsigned r,
+                                             u64 E, u64 cap) {
+    if (threadIdx.x != 0) return;
+    __threadfence();
+    const unsigned done = atomicAdd(&C->exits, 1u);
+    if (done != gridDim.x - 1) return;
+    __threadfence();
+    C->exits = 0;
+    RoundStats& rs = C->rs[r];
+    const u64 unique = *reinterpret_cast<volatile u64*>(&rs.unique);
+    const u64 emitted = unique < cap ? unique : cap;
+    if (emitted > B.layer_cap) {
+        C->need = emitted;
+        C->abort = kGrowLayer;
+        return;
+    }
+    rs.expanded = E;
+    rs.emitted = emitted;
+    rs.overflowed = unique > cap ? 1u : 0u;
+    rs.valid = 1;
+    C->count[(r + 1) & 1] = emitted;
+    C->round = r + 1;
+    C->epoch = (C->epoch & kEpochMask) == kEpochMask ? 1 : C->epoch + 1;
+    if (emitted == 0 || static_cast<int>(r) + 1 >= P->rounds) C->stop = 1;
 }
 
 template <int W, bool PROBE>
@@ -729,6 +763,7 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
     __shared__ u64 s_tile;
     if (halted(C)) return;
     const unsigned r = C->round;
+    const unsigned epoch = C->epoch;
     const u64 E = C->count[r & 1];
     const u64 ntiles = (E + kThreads - 1) / kThreads;
     const u64 cap = round_cap(*P, E);
@@ -743,7 +778,7 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
     unsigned* hout = B.hist[(r + 1) & 1];
 
     for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&C->ticket, 1u);
+        if (threadIdx.x == 0) s_tile = atomicAdd(&C->rs[r].ticket, 1ull);
         __syncthreads();
         const u64 tile = s_tile;
         if (tile >= ntiles) break;
@@ -784,29 +819,10 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
         const unsigned cnt = static_cast<unsigned>(M.count());
         unsigned excl_block, total_block;
         BlockScan(scan_tmp).ExclusiveSum(cnt, excl_block, total_block);
-        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, tile, total_block);
+        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, tile, total_block, epoch);
         __syncthreads();
         const u64 prefix = s_prefix;
-        // coalesced writes: the warp's survivors occupy one contiguous run
-        WarpFlat f;
-        f.scan(static_cast<int>(cnt));
-        const u64 warp_start = prefix + __shfl_sync(kFull, excl_block, 0);
-        for (int t = 0; t < f.total; t += 32) {
-            const int j = t + lane;
-            const int src = f.source(j);
-            const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
-            const Set<W> Ms = shfl_set<W>(M, src);
-            const Set<W> Ss = shfl_set<W>(S, src);
-            const unsigned Hs = __shfl_sync(kFull, H, src);
-            const u64 pos = warp_start + j;
-            if (j < f.total && pos < limit) {
-                const int v = nth_member<W>(Ms, j - excl);
-                Set<W> key = Ss;
-                key.add(v);
-                store_set<W>(out, pos, key);
-                hout[pos] = (Hs << 8) | static_cast<unsigned>(v & 0xFF);  // push_history
-            }
-        }
+        append_survivors<W>(M, S, H, prefix + __shfl_sync(kFull, excl_block, 0), limit, out, hout);
         if (threadIdx.x == 0 && tile == ntiles - 1) {
             // the final tile knows the round's survivor total
             const u64 unique = prefix + total_block;
@@ -814,31 +830,186 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
         }
         __syncthreads();
     }
-    // the last CTA out publishes the round (all CTAs have read the round
-    // state by now, so advancing it cannot race with a late starter)
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned done = atomicAdd(&C->exits, 1u);
-        if (done == gridDim.x - 1) {
-            __threadfence();
-            C->exits = 0;
-            RoundStats& rs = C->rs[r];
-            const u64 unique = *reinterpret_cast<volatile u64*>(&rs.unique);
-            const u64 emitted = unique < cap ? unique : cap;
-            if (emitted > B.layer_cap) {
-                C->need = emitted;
-                C->abort = kGrowLayer;
-            } else {
-                rs.expanded = E;
-                rs.emitted = emitted;
-                rs.overflowed = unique > cap ? 1u : 0u;
-                rs.valid = 1;
-                C->count[(r + 1) & 1] = emitted;
-                C->round = r + 1;
-                if (emitted == 0 || static_cast<int>(r) + 1 >= P->rounds) C->stop = 1;
-            }
+    finish_round(P, C, B, r, E, cap);
+}
+
+// ----------------------------------------------------------------------
+// Fused Bloom round (replaces expand_range + the Bloom branch of
+// expand_layer, dp.cpp:39-69 + 93-117): per 256-parent tile
+//   K1 candidates -> block-local exact dedup in shared memory -> global
+//   Bloom insert (fast read-only path, else stripe lock + 17 atomicOr) ->
+//   decoupled look-back scan -> rank-ordered append.
+// Two Bloom filters alternate by round parity; while round r fills filter
+// r&1, its CTAs clear the region round r-1 used in the other filter, so no
+// separate clear pass (or launch) is needed.
+
+constexpr int kLocalBytes = 32 * 1024;  // dynamic shared memory for the tile's key set
+
+// Block-shared open-addressing set of child keys (key 0 = empty: children
+// are never the empty set). Returns true for the first inserter of a key in
+// the tile, and also when the probe budget runs out (the global filter then
+// decides), so a crowded table only costs dedup efficiency, never states.
+template <int W>
+__device__ __forceinline__ bool local_first(u64* slots, unsigned mask, const Set<W>& key) {
+    unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & mask;
+    for (int probe = 0; probe < 32; ++probe) {
+        if constexpr (W == 1) {
+            const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(slots + h), 0ull, key.w[0]);
+            if (prev == 0) return true;
+            if (prev == key.w[0]) return false;
+        } else {
+            u64 lo, hi;
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(slots + 2 * h));
+            asm volatile(
+                "{\n\t.reg .b128 c, s, d;\n\t"
+                "mov.b128 c, {%2, %3};\n\t"
+                "mov.b128 s, {%4, %5};\n\t"
+                "atom.shared.cas.b128 d, [%6], c, s;\n\t"
+                "mov.b128 {%0, %1}, d;\n\t}"
+                : "=l"(lo), "=l"(hi)
+                : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
+                : "memory");
+            if ((lo | hi) == 0) return true;
+            if (lo == key.w[0] && hi == key.w[1]) return false;
         }
+        h = (h + 1) & mask;
     }
+    return true;
+}
+
+// Position of the child number j of the tile: binary search over the
+// block-inclusive child counts in shared memory (first parent whose
+// inclusive count exceeds j).
+__device__ __forceinline__ int tile_source(const unsigned* incl, unsigned j) {
+    int lo = 0;
+#pragma unroll
+    for (int step = kThreads / 2; step >= 1; step >>= 1)
+        if (incl[lo + step - 1] <= j) lo += step;
+    return lo;
+}
+
+template <int W, bool MMW>
+__global__ void __launch_bounds__(kThreads, 3) k_round_bloom(const Params* __restrict__ P, Control* C,
+                                                             Bufs B) {
+    using BlockScan = cub::BlockScan<unsigned, kThreads>;
+    extern __shared__ __align__(16) u64 local_slots[];
+    __shared__ typename BlockScan::TempStorage scan_tmp;
+    __shared__ Set<W> adj[64 * W];
+    __shared__ Set<W> t_set[kThreads];     // parents of the tile
+    __shared__ Set<W> t_mask[kThreads];    // their candidates, then their novel children
+    __shared__ unsigned t_hist[kThreads];
+    __shared__ unsigned t_incl[kThreads];  // inclusive child counts
+    __shared__ unsigned novel_words[kThreads][2 * W];
+    __shared__ u64 s_prefix;
+    __shared__ u64 s_tile;
+    if (halted(C)) return;
+    const unsigned r = C->round;
+    const unsigned epoch = C->epoch;
+    const u64 E = C->count[r & 1];
+    const u64 cap = round_cap(*P, E);
+    const u64 m = bloom_bits_for(cap, P->bpe);
+    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+    const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
+    if (m / 32 > B.bloom_cap) {
+        if (gtid == 0) {
+            C->need = m / 32;
+            C->abort = kGrowBloom;
+        }
+        return;
+    }
+    // clear the other filter's region from round r-1 (needed clean at r+1)
+    if (r > 0) {
+        const u64 prev_words = bloom_bits_for(round_cap(*P, C->rs[r - 1].expanded), P->bpe) / 32;
+        uint4* w4 = reinterpret_cast<uint4*>(B.bloom[(r + 1) & 1]);
+        const u64 n4 = prev_words / 4;
+        for (u64 i = gtid; i < n4; i += gstride) w4[i] = make_uint4(0, 0, 0, 0);
+        for (u64 i = n4 * 4 + gtid; i < prev_words; i += gstride) B.bloom[(r + 1) & 1][i] = 0;
+    }
+    unsigned* bits = B.bloom[r & 1];
+    load_adjacency<W>(P, adj);
+    const u64 ntiles = (E + kThreads - 1) / kThreads;
+    const u64 limit = cap < B.layer_cap ? cap : B.layer_cap;
+    constexpr unsigned kSlots = kLocalBytes / (8 * W);
+    const Set<W> forbidden = param_set<W>(P->forbidden);
+    const bool single_lock = (P->flags & 2) != 0;
+    const u64* in = B.keys[r & 1];
+    const unsigned* hin = B.hist[r & 1];
+    u64* out = B.keys[(r + 1) & 1];
+    unsigned* hout = B.hist[(r + 1) & 1];
+    u64 offered = 0, pruned = 0;
+
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&C->rs[r].ticket, 1ull);
+        for (unsigned i = threadIdx.x; i < kSlots * W; i += kThreads) local_slots[i] = 0;
+#pragma unroll
+        for (int i = 0; i < 2 * W; ++i) novel_words[threadIdx.x][i] = 0;
+        __syncthreads();
+        const u64 tile = s_tile;
+        if (tile >= ntiles) break;
+        const u64 idx = tile * kThreads + threadIdx.x;
+        const bool valid = idx < E;
+        const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
+        const Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned)
+                               : Set<W>::zero();
+        t_set[threadIdx.x] = S;
+        t_mask[threadIdx.x] = M;
+        t_hist[threadIdx.x] = valid ? hin[idx] : 0u;
+        unsigned incl, children;
+        BlockScan(scan_tmp).InclusiveSum(static_cast<unsigned>(M.count()), incl, children);
+        t_incl[threadIdx.x] = incl;
+        offered += M.count();
+        __syncthreads();
+        // dedup: children spread evenly over the block (block-level flattening)
+        for (unsigned j = threadIdx.x; j < children; j += kThreads) {
+            const int src = tile_source(t_incl, j);
+            const unsigned before = src ? t_incl[src - 1] : 0u;
+            const int v = nth_member<W>(t_mask[src], static_cast<int>(j - before));
+            Set<W> key = t_set[src];
+            key.add(v);
+            if (local_first<W>(local_slots, kSlots - 1, key) &&
+                bloom_insert<W>(bits, B.locks, m, P->hashes, key, single_lock))
+                atomicOr(&novel_words[src][v >> 5], 1u << (v & 31));
+        }
+        __syncthreads();
+        Set<W> N;
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            N.w[i] = novel_words[threadIdx.x][2 * i] |
+                     (static_cast<u64>(novel_words[threadIdx.x][2 * i + 1]) << 32);
+        t_mask[threadIdx.x] = N;
+        unsigned nincl, survivors;
+        __syncthreads();  // scan_tmp reuse
+        BlockScan(scan_tmp).InclusiveSum(static_cast<unsigned>(N.count()), nincl, survivors);
+        t_incl[threadIdx.x] = nincl;
+        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, tile, survivors, epoch);
+        __syncthreads();
+        // rank-ordered append, consecutive threads store consecutive states
+        const u64 prefix = s_prefix;
+        for (unsigned j = threadIdx.x; j < survivors; j += kThreads) {
+            const u64 pos = prefix + j;
+            if (pos >= limit) break;  // capacity wall: drop the newest (dp.cpp:107,152-155)
+            const int src = tile_source(t_incl, j);
+            const unsigned before = src ? t_incl[src - 1] : 0u;
+            const int v = nth_member<W>(t_mask[src], static_cast<int>(j - before));
+            Set<W> key = t_set[src];
+            key.add(v);
+            store_set<W>(out, pos, key);
+            hout[pos] = (t_hist[src] << 8) | static_cast<unsigned>(v & 0xFF);  // push_history
+        }
+        if (threadIdx.x == 0 && tile == ntiles - 1) C->rs[r].unique = prefix + survivors;
+        __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        offered += __shfl_xor_sync(kFull, offered, o);
+        pruned += __shfl_xor_sync(kFull, pruned, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (offered) atomicAdd(&C->rs[r].offered, offered);
+        if (pruned) atomicAdd(&C->rs[r].mmw_pruned, pruned);
+    }
+    __syncthreads();
+    finish_round(P, C, B, r, E, cap);
 }
 
 // ----------------------------------------------------------------------
@@ -996,7 +1167,8 @@ public:
         const u64 count = keys.size() / words;
         const u64 m = bloom_bits_for(expected, bpe);
         ensure_bloom(m / 32);
-        check(cudaMemsetAsync(b_.bloom, 0, (m / 32) * 4, stream_), "bloom zero");
+        check(cudaMemsetAsync(b_.bloom[0], 0, (m / 32) * 4, stream_), "bloom zero");
+        bloom_dirty_[0] = std::max<u64>(bloom_dirty_[0], m / 32);
         u64* d_keys = nullptr;
         unsigned char* d_novel = nullptr;
         check(cudaMalloc(&d_keys, std::max<u64>(8, keys.size() * 8)), "keys");
@@ -1005,10 +1177,10 @@ public:
         const int blocks = static_cast<int>((count + 255) / 256);
         if (count) {
             if (words == 1)
-                k_bloom_batch<1><<<blocks, 256, 0, stream_>>>(d_keys, count, b_.bloom, b_.locks, m,
+                k_bloom_batch<1><<<blocks, 256, 0, stream_>>>(d_keys, count, b_.bloom[0], b_.locks, m,
                                                              hashes, d_novel);
             else
-                k_bloom_batch<2><<<blocks, 256, 0, stream_>>>(d_keys, count, b_.bloom, b_.locks, m,
+                k_bloom_batch<2><<<blocks, 256, 0, stream_>>>(d_keys, count, b_.bloom[0], b_.locks, m,
                                                              hashes, d_novel);
             check(cudaGetLastError(), "bloom batch");
             prof.t.kernel_launches++;
@@ -1018,7 +1190,7 @@ public:
             copy(novel.data(), d_novel, count, cudaMemcpyDeviceToHost, "novel d2h");
         if (bits) {
             bits->assign(m / 32, 0);
-            copy(bits->data(), b_.bloom, (m / 32) * 4, cudaMemcpyDeviceToHost, "bits d2h");
+            copy(bits->data(), b_.bloom[0], (m / 32) * 4, cudaMemcpyDeviceToHost, "bits d2h");
         }
         check(cudaStreamSynchronize(stream_), "sync");
         cudaFree(d_keys);
@@ -1036,6 +1208,24 @@ private:
     Control* h_ctl_ = nullptr;
     Bufs b_{};
     u64 table_dirty_bytes_ = 0;  // table bytes possibly holding keys of an earlier decide
+    u64 bloom_dirty_[2] = {0, 0};  // words of each Bloom filter that may hold bits
+    unsigned epoch_ = 1;          // look-back epoch carried across decides
+    bool bloom_round_ = false;    // current decide runs the fused Bloom round
+    int grid_fused_ = 0;
+
+    // Epochs tag look-back statuses (24 bits); on wrap-around the status
+    // array is cleared so a status from 2^24 attempts ago cannot match.
+    unsigned next_epoch() {
+        epoch_ = (epoch_ + 1) & kEpochMask;
+        if (epoch_ == 0) {
+            epoch_ = 1;
+            if (b_.tiles)
+                check(cudaMemsetAsync(b_.tiles, 0, ((b_.layer_cap + kThreads - 1) / kThreads + 1) * 8,
+                                      stream_),
+                      "tiles clear");
+        }
+        return epoch_;
+    }
     int table_layout_ = 0;       // slot layout (W) the clean part of the table is in
     int grid_ = 0;
     cudaEvent_t ev_[2] = {nullptr, nullptr};
@@ -1064,6 +1254,20 @@ private:
         info_.sm_count = prop.multiProcessorCount;
         std::snprintf(info_.name, sizeof info_.name, "%s", prop.name);
         grid_ = prop.multiProcessorCount * 4;
+        // fused Bloom round: 64 KB of dynamic shared memory per CTA
+        auto allow = [&](auto kernel) {
+            check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLocalBytes),
+                  "smem attribute");
+        };
+        allow(k_round_bloom<1, false>);
+        allow(k_round_bloom<1, true>);
+        allow(k_round_bloom<2, false>);
+        allow(k_round_bloom<2, true>);
+        int per_sm = 0;
+        check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_round_bloom<1, false>, kThreads,
+                                                            kLocalBytes),
+              "occupancy");
+        grid_fused_ = prop.multiProcessorCount * std::max(1, per_sm);
         check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
         check(cudaMalloc(&d_params_, sizeof(Params)), "malloc params");
         check(cudaMallocHost(&h_params_, sizeof(Params)), "host params");
@@ -1110,6 +1314,7 @@ private:
         Control& c = *h_ctl_;
         std::memset(&c, 0, sizeof c);
         c.count[0] = first_count;
+        c.epoch = next_epoch();
         copy(d_ctl_, h_ctl_, sizeof(Control), cudaMemcpyHostToDevice, "control");
     }
 
@@ -1144,6 +1349,7 @@ private:
         if (b_.tiles) cudaFree(b_.tiles);
         check(cudaMalloc(&b_.cmask, cap * 16), "cmask");
         check(cudaMalloc(&b_.tiles, ((cap + kThreads - 1) / kThreads + 1) * 8), "tiles");
+        check(cudaMemsetAsync(b_.tiles, 0, ((cap + kThreads - 1) / kThreads + 1) * 8, stream_), "tiles");
         b_.layer_cap = cap;
     }
 
@@ -1158,11 +1364,32 @@ private:
     }
 
     void ensure_bloom(u64 words) {
-        if (words <= b_.bloom_cap && b_.bloom) return;
+        if (words <= b_.bloom_cap && b_.bloom[0]) return;
         u64 cap = std::max<u64>(words, u64{1} << 22);
-        if (b_.bloom) cudaFree(b_.bloom);
-        check(cudaMalloc(&b_.bloom, cap * 4), "bloom");
+        for (int f = 0; f < 2; ++f) {
+            if (b_.bloom[f]) cudaFree(b_.bloom[f]);
+            check(cudaMalloc(&b_.bloom[f], cap * 4), "bloom");
+            check(cudaMemsetAsync(b_.bloom[f], 0, cap * 4, stream_), "bloom zero");
+            bloom_dirty_[f] = 0;
+        }
         b_.bloom_cap = cap;
+    }
+
+    // Bloom filters must be all-zero when a decide starts; the fused round
+    // kernel keeps them clean within a decide, this covers what is left.
+    void clean_blooms() {
+        for (int f = 0; f < 2; ++f) {
+            if (!bloom_dirty_[f]) continue;
+            const u64 words = std::min(bloom_dirty_[f], b_.bloom_cap);
+            check(cudaMemsetAsync(b_.bloom[f], 0, words * 4, stream_), "bloom clean");
+            bloom_dirty_[f] = 0;
+        }
+    }
+
+    u64 host_round_cap(u64 e_in) const {
+        u64 upper = e_in * static_cast<u64>(h_params_->free_count);
+        if (upper < 1) upper = 1;
+        return std::min<u64>(h_params_->max_states, upper);
     }
 
     // The "empty" pattern differs between the 16-byte (W=1) and 32-byte
@@ -1205,36 +1432,48 @@ private:
                 ms += t;
             }
         };
-        if (!exact)
-            timed_launch([&] { k_bloom_clear<<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
-                         prof.t.clear_ms, prof.t.clear_launches);
+        if (!exact) {
+            if (cfg.use_mmw)
+                timed_launch([&] { k_round_bloom<W, true><<<grid_fused_, kThreads, kLocalBytes, stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.fused_ms, prof.t.fused_launches);
+            else
+                timed_launch([&] { k_round_bloom<W, false><<<grid_fused_, kThreads, kLocalBytes, stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.fused_ms, prof.t.fused_launches);
+            return;
+        }
         if (cfg.use_mmw)
             timed_launch([&] { k_expand<W, true><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
         else
             timed_launch([&] { k_expand<W, false><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
-        if (exact) {
-            timed_launch([&] { k_exact_insert<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
-                         prof.t.insert_ms, prof.t.insert_launches);
-            timed_launch([&] { k_append<W, true><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
-                         prof.t.append_ms, prof.t.append_launches);
-        } else {
-            timed_launch([&] { k_bloom_insert<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
-                         prof.t.insert_ms, prof.t.insert_launches);
-            timed_launch([&] { k_append<W, false><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
-                         prof.t.append_ms, prof.t.append_launches);
-        }
+        timed_launch([&] { k_exact_insert<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
+                     prof.t.insert_ms, prof.t.insert_launches);
+        timed_launch([&] { k_append<W, true><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
+                     prof.t.append_ms, prof.t.append_launches);
     }
 
     void fetch_control() {
         copy(h_ctl_, d_ctl_, sizeof(Control), cudaMemcpyDeviceToHost, "control d2h");
         check(cudaStreamSynchronize(stream_), "sync");
+        // the device advanced the look-back epoch once per round; continue
+        // from there (a wrap past 2^24 clears the status array)
+        if (h_ctl_->epoch < epoch_) {
+            epoch_ = h_ctl_->epoch;
+            if (b_.tiles)
+                check(cudaMemsetAsync(b_.tiles, 0, ((b_.layer_cap + kThreads - 1) / kThreads + 1) * 8,
+                                      stream_),
+                      "tiles clear");
+        } else {
+            epoch_ = h_ctl_->epoch;
+        }
     }
 
     void run_rounds(int W, const DpConfig& cfg, int rounds, int k, const LayerObserver* observer) {
         ensure_table(u64{1} << 20);
         ensure_bloom(u64{1} << 22);
+        bloom_round_ = cfg.dedup == DedupMode::bloom;
+        if (bloom_round_) clean_blooms();
         if (!prof.on) check(cudaEventRecord(ev_[0], stream_), "event");
         auto t0 = std::chrono::steady_clock::now();
         const bool sync_each = (h_params_->flags & 8) != 0;
@@ -1262,6 +1501,15 @@ private:
             if (c.stop || static_cast<int>(c.round) >= rounds) break;
             if (!observer && !sync_each) chunk = std::min(chunk * 2, 32);  // observer: one round per check
         }
+        if (bloom_round_) {  // the last round's filter is left dirty
+            int last = -1;
+            for (int r = 0; r < rounds; ++r)
+                if (h_ctl_->rs[r].valid) last = r;
+            if (last >= 0)
+                bloom_dirty_[last & 1] = std::max<u64>(
+                    bloom_dirty_[last & 1],
+                    bloom_bits_for(host_round_cap(h_ctl_->rs[last].expanded), h_params_->bpe) / 32);
+        }
         if (cfg.dedup == DedupMode::exact_set) {
             const u64 slot_bytes = W == 1 ? 16 : 32;
             for (int r = 0; r < rounds; ++r)
@@ -1287,6 +1535,12 @@ private:
         switch (c.abort) {
             case kGrowLayer:
                 ensure_layers(c.need + c.need / 2, static_cast<int>(r & 1), c.count[r & 1]);
+                if (bloom_round_) {  // the aborted attempt left bits in filter r&1
+                    bloom_dirty_[r & 1] = std::max<u64>(
+                        bloom_dirty_[r & 1],
+                        bloom_bits_for(host_round_cap(c.count[r & 1]), h_params_->bpe) / 32);
+                    clean_blooms();
+                }
                 break;
             case kGrowTable:
                 ensure_table(c.need);  // fresh memory, fully reset below
@@ -1301,8 +1555,8 @@ private:
         // re-arm: clear the abort and the partial statistics of round r
         c.abort = kOk;
         c.need = 0;
-        c.ticket = 0;
         c.exits = 0;
+        c.epoch = next_epoch();  // statuses of the aborted attempt must not match
         std::memset(&c.rs[r], 0, sizeof(RoundStats) * (kMaxRounds - r));
         copy(d_ctl_, h_ctl_, sizeof(Control), cudaMemcpyHostToDevice, "control re-arm");
     }
