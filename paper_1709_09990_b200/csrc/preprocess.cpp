@@ -2,7 +2,6 @@
 
 #include <algorithm>
 #include <array>
-#include <deque>
 #include <functional>
 
 namespace etw {
@@ -145,67 +144,74 @@ void grow_clique(const Graph& g, std::vector<int>& cur, HostSet cand, std::vecto
 }
 
 // Maximum number of internally vertex-disjoint s-t paths (s, t
-// non-adjacent): unit vertex capacities via the usual in/out split, BFS
-// augmenting paths. The value is a max-flow value, hence independent of the
-// augmentation order (the reference uses Dinic, preprocess.cpp:115-169).
-class VertexFlow {
+// non-adjacent), by augmenting paths in the vertex-split residual graph.
+// The residual arcs are derived from bitsets instead of an arc list:
+//   out(u) -> in(w)  for every edge uw (infinite capacity),
+//   out(u) -> in(u)  when u carries a path (reverse of the vertex arc),
+//   in(v)  -> out(v) when v is still free,
+//   in(v)  -> out(u) when a path enters v from u (reverse flow arc).
+// The value is a max-flow value, hence independent of the augmentation
+// order (the reference runs Dinic on an explicit network, preprocess.cpp:
+// 115-169, 218-243).
+class MengerFlow {
 public:
-    explicit VertexFlow(const Graph& g) : g_(g), n_(g.vertex_count()) {
-        // node 2v = in(v), 2v+1 = out(v)
-        int nodes = 2 * n_;
-        head_.assign(nodes, -1);
-        for (int v = 0; v < n_; ++v) add_arc(2 * v, 2 * v + 1, 1);
-        for (int v = 0; v < n_; ++v)
-            for (int u : g.neighbor_list(v)) add_arc(2 * v + 1, 2 * u, kBig);
-        base_cap_ = cap_;
-    }
+    explicit MengerFlow(const Graph& g) : g_(g), n_(g.vertex_count()), into_(n_), par_in_(n_), par_out_(n_) {}
 
     int paths(int s, int t) {
-        cap_ = base_cap_;
-        int src = 2 * s + 1, dst = 2 * t;
+        used_ = HostSet::zero();
+        for (HostSet& x : into_) x = HostSet::zero();
         int flow = 0;
-        std::vector<int> via(2 * n_);
-        for (;;) {
-            std::fill(via.begin(), via.end(), -2);
-            std::deque<int> q{src};
-            via[src] = -1;
-            while (!q.empty() && via[dst] == -2) {
-                int x = q.front();
-                q.pop_front();
-                for (int a = head_[x]; a >= 0; a = next_[a]) {
-                    int y = to_[a];
-                    if (cap_[a] > 0 && via[y] == -2) {
-                        via[y] = a;
-                        q.push_back(y);
-                    }
-                }
-            }
-            if (via[dst] == -2) return flow;
-            for (int y = dst; y != src;) {
-                int a = via[y];
-                cap_[a] -= 1;
-                cap_[a ^ 1] += 1;
-                y = to_[a ^ 1];
-            }
-            ++flow;
-        }
+        while (augment(s, t)) ++flow;
+        return flow;
     }
 
 private:
-    static constexpr int kBig = 1 << 20;
-    void add_arc(int a, int b, int c) {
-        to_.push_back(b);
-        cap_.push_back(c);
-        next_.push_back(head_[a]);
-        head_[a] = static_cast<int>(to_.size()) - 1;
-        to_.push_back(a);
-        cap_.push_back(0);
-        next_.push_back(head_[b]);
-        head_[b] = static_cast<int>(to_.size()) - 1;
+    bool augment(int s, int t) {
+        HostSet seen_in = HostSet::zero(), seen_out = HostSet::bit(s);
+        HostSet frontier_out = seen_out;
+        for (;;) {
+            HostSet reached_in = HostSet::zero();
+            for (int u : members(frontier_out)) {
+                HostSet c = g_.neighbors(u);
+                if (used_.has(u)) c.add(u);
+                c = c - seen_in;
+                for (int v : members(c)) par_in_[v] = u;
+                seen_in |= c;
+                reached_in |= c;
+            }
+            if (seen_in.has(t)) break;
+            HostSet reached_out = HostSet::zero();
+            for (int v : members(reached_in)) {
+                HostSet c = into_[v];
+                if (!used_.has(v)) c.add(v);
+                c = c - seen_out;
+                for (int x : members(c)) par_out_[x] = v;
+                seen_out |= c;
+                reached_out |= c;
+            }
+            if (reached_out.none()) return false;
+            frontier_out = reached_out;
+        }
+        // walk the path back from in(t), updating the flow
+        int x_in = t;
+        for (;;) {
+            const int u = par_in_[x_in];  // arc out(u) -> in(x_in)
+            if (u == x_in) used_.del(u);  // reverse vertex arc: u is freed
+            else into_[x_in].add(u);      // forward edge arc
+            if (u == s) break;
+            const int v = par_out_[u];    // arc in(v) -> out(u)
+            if (v == u) used_.add(u);     // forward vertex arc: u now carries a path
+            else into_[v].del(u);         // reverse flow arc: cancels u -> v
+            x_in = v;
+        }
+        return true;
     }
+
     const Graph& g_;
     int n_;
-    std::vector<int> head_, next_, to_, cap_, base_cap_;
+    HostSet used_ = HostSet::zero();
+    std::vector<HostSet> into_;  // into_[v] = vertices u with a path arc u -> v
+    std::vector<int> par_in_, par_out_;
 };
 
 }  // namespace
@@ -234,15 +240,18 @@ HostSet max_clique(const Graph& g) {
     return c;
 }
 
-PathCounts disjoint_path_counts(const Graph& g) {
+PathCounts disjoint_path_counts(const Graph& g, int need) {
     int n = g.vertex_count();
     PathCounts pc;
     pc.n = n;
     pc.counts.assign(static_cast<size_t>(n) * n, 0);
-    VertexFlow flow(g);
+    MengerFlow flow(g);
     for (int s = 0; s < n; ++s)
         for (int t = s + 1; t < n; ++t) {
-            int c = g.adjacent(s, t) ? PathCounts::kAdjacent : flow.paths(s, t);
+            // at most min(deg s, deg t) paths: below `need` that bound decides
+            const int bound = std::min(g.neighbors(s).count(), g.neighbors(t).count());
+            int c = g.adjacent(s, t) ? PathCounts::kAdjacent
+                                     : (bound < need ? bound : flow.paths(s, t));
             pc.counts[static_cast<size_t>(s) * n + t] = static_cast<uint8_t>(c);
             pc.counts[static_cast<size_t>(t) * n + s] = static_cast<uint8_t>(c);
         }

@@ -37,7 +37,9 @@ struct PathCounts {
     std::vector<uint8_t> counts;
     int at(int u, int v) const { return counts[static_cast<size_t>(u) * n + v]; }
 };
-PathCounts disjoint_path_counts(const Graph& g);
+// Pairs whose degree bound min(deg u, deg v) is below `need` get that bound
+// instead of the exact count (enough for improve_graph at any k >= need-1).
+PathCounts disjoint_path_counts(const Graph& g, int need = 0);
 
 // Adds every non-edge {u,v} joined by >= k+1 disjoint paths
 // (preprocess.cpp:245-258).
