@@ -220,10 +220,10 @@ def roofline(p):
     append: 12 B per parent read + 12 B per state written)."""
     peak, peak_src = peaks()
     classes = {
-        # fused Bloom round: the whole SURVEY §8d round, B = W*E_in + W*E_out + D*P
-        "k_round_bloom": (p["fused_ms"], p["fused_launches"], p["layer_bytes"] + p["dedup_bytes"]),
+        # Bloom pass 1: candidates + dedup, D = 4h = 68 B per offered child
+        # plus the parent read and the mask write (2 x 8 B per parent)
+        "k_bloom_dedup": (p["insert_ms"], p["insert_launches"], p["dedup_bytes"] + 16.0 * p["expanded"]),
         "k_expand": (p["expand_ms"], p["expand_launches"], 16.0 * p["expanded"]),
-        "k_bloom_insert": (p["insert_ms"], p["insert_launches"], p["dedup_bytes"]),
         "k_append": (p["append_ms"], p["append_launches"], p["layer_bytes"]),
         "k_bloom_clear": (p["clear_ms"], p["clear_launches"], None),
     }

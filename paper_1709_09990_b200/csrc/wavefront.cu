@@ -4,7 +4,7 @@
 // mmw.cpp:20-146).
 //
 // Per round (one BFS layer of the Held-Karp prefix DP) the device runs:
-//   bloom : k_round_bloom (one fused kernel per round)
+//   bloom : k_bloom_dedup -> k_append<mask>
 //   exact : k_expand -> k_exact_insert -> k_append<probe>
 //
 //   k_expand       one thread per parent S. The components of G[S] are
@@ -65,7 +65,7 @@ struct RoundStats {
     unsigned overflowed, valid;
 };
 
-enum AbortCode : unsigned { kOk = 0, kGrowLayer = 1, kGrowTable = 2, kGrowBloom = 3 };
+enum AbortCode : unsigned { kOk = 0, kGrowLayer = 1, kGrowTable = 2, kGrowBloom = 3, kGrowClaims = 4 };
 
 struct Control {
     u64 count[2];       // layer sizes, ping-pong by round parity
@@ -98,6 +98,8 @@ struct Bufs {
     u64 layer_cap;   // states per layer buffer
     u64 table_cap;   // slots
     u64 bloom_cap;   // 32-bit words
+    u64* claims;     // Bloom-mode claim table, 16-byte {key, epoch} slots
+    u64 claim_cap;   // slots
 };
 
 // ----------------------------------------------------------------------
@@ -659,6 +661,216 @@ __global__ void k_bloom_batch(const u64* keys, u64 count, unsigned* bits, unsign
 }
 
 // ----------------------------------------------------------------------
+// Bloom round, pass 1 (replaces expand_range + the Bloom branch of
+// expand_layer, dp.cpp:39-69 + 93-117), barrier-free: each warp takes 32
+// consecutive parents, evaluates their candidates (K1), flattens the
+// children over its lanes, drops duplicates among them with a warp-private
+// shared-memory key set (siblings of one grandparent sit next to each other
+// in the layer, so most duplicates are local), and sends the rest to the
+// global Bloom filter. The novel-children mask of every parent goes to HBM;
+// pass 2 (k_append<W,false>) turns masks into the rank-ordered next layer.
+//
+// Exactly-once novelty without the stripe-lock fences: an insert sets its
+// 17 bits with relaxed atomicOr; if any was clear it *claims* the key in an
+// epoch-tagged table with one 128-bit CAS — of several concurrent inserters
+// of the same key exactly one claim succeeds (the reference's lock-based
+// guarantee, bloom.cpp:86-97). W=2 keys (16 bytes + tag) do not fit a
+// 16-byte CAS and use the reference's stripe locks, as does any round whose
+// claim table would exceed kClaimMax.
+
+constexpr int kWarpLocalBytes = 4096;               // per-warp key set
+constexpr int kLocalBytes = kWarpLocalBytes * (kThreads / 32);
+constexpr u64 kClaimMax = u64{1} << 27;             // slots (16 B each)
+
+// Warp-private open-addressing set (key 0 = empty; children are never the
+// empty set). True for the first inserter, and when the probe budget runs
+// out (the global filter then decides: costs dedup efficiency, never states).
+template <int W>
+__device__ __forceinline__ bool local_first(u64* slots, unsigned mask, const Set<W>& key) {
+    unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & mask;
+    for (int probe = 0; probe < 16; ++probe) {
+        if constexpr (W == 1) {
+            const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(slots + h), 0ull, key.w[0]);
+            if (prev == 0) return true;
+            if (prev == key.w[0]) return false;
+        } else {
+            u64 lo, hi;
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(slots + 2 * h));
+            asm volatile(
+                "{\n\t.reg .b128 c, s, d;\n\t"
+                "mov.b128 c, {%2, %3};\n\t"
+                "mov.b128 s, {%4, %5};\n\t"
+                "atom.shared.cas.b128 d, [%6], c, s;\n\t"
+                "mov.b128 {%0, %1}, d;\n\t}"
+                : "=l"(lo), "=l"(hi)
+                : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
+                : "memory");
+            if ((lo | hi) == 0) return true;
+            if (lo == key.w[0] && hi == key.w[1]) return false;
+        }
+        h = (h + 1) & mask;
+    }
+    return true;
+}
+
+// Claims a 64-bit key for this round attempt (tag = epoch) in the
+// open-addressing claim table; true iff this call is the first claim.
+__device__ __forceinline__ bool claim_key(u64* claims, u64 mask, u64 key, u64 tag) {
+    u64 i = fmix64(key ^ 0x9E3779B97F4A7C15ULL) & mask;
+    for (;;) {
+        u64* slot = claims + 2 * i;
+        u64 lo, hi;
+        cas128(slot, ~u64{0}, ~u64{0}, ~u64{0}, ~u64{0}, lo, hi);  // untorn read
+        for (;;) {
+            if (hi == tag) {
+                if (lo == key) return false;
+                break;  // another key of this round: probe on
+            }
+            u64 plo, phi;
+            cas128(slot, lo, hi, key, tag, plo, phi);
+            if (plo == lo && phi == hi) return true;
+            lo = plo;
+            hi = phi;
+        }
+        i = (i + 1) & mask;
+    }
+}
+
+// Sets the key's probe bits (relaxed atomicOr); true when one was clear.
+template <int H>
+__device__ __forceinline__ bool bloom_set_bits(unsigned* bits, u64 m, u64 first, u64 step) {
+    unsigned pos[H];
+    unsigned word[H];
+    const unsigned m32 = static_cast<unsigned>(m), step32 = static_cast<unsigned>(step);
+    pos[0] = static_cast<unsigned>(first);
+#pragma unroll
+    for (int i = 1; i < H; ++i) {
+        const unsigned p = pos[i - 1] + step32;
+        pos[i] = (p >= m32 || p < pos[i - 1]) ? p - m32 : p;
+    }
+#pragma unroll
+    for (int i = 0; i < H; ++i) word[i] = __ldcg(bits + (pos[i] >> 5));
+    bool all_set = true;
+#pragma unroll
+    for (int i = 0; i < H; ++i) all_set &= ((word[i] >> (pos[i] & 31)) & 1u) != 0;
+    if (all_set) return false;  // duplicate (or false positive) in any serialisation
+#pragma unroll
+    for (int i = 0; i < H; ++i) word[i] = atomicOr(bits + (pos[i] >> 5), 1u << (pos[i] & 31));
+    bool any_clear = false;
+#pragma unroll
+    for (int i = 0; i < H; ++i) any_clear |= ((word[i] >> (pos[i] & 31)) & 1u) == 0;
+    return any_clear;
+}
+
+template <int W, bool MMW>
+__global__ void __launch_bounds__(kThreads, 3) k_bloom_dedup(const Params* __restrict__ P, Control* C,
+                                                          Bufs B) {
+    extern __shared__ __align__(16) u64 local_slots[];
+    __shared__ Set<W> adj[64 * W];
+    __shared__ unsigned novel_words[kThreads][2 * W];
+    if (halted(C)) return;
+    const unsigned r = C->round;
+    const unsigned epoch = C->epoch;
+    const u64 E = C->count[r & 1];
+    const u64 cap = round_cap(*P, E);
+    const u64 m = bloom_bits_for(cap, P->bpe);
+    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+    const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
+    // claim table sized for every key the round can offer (E_in * free)
+    const u64 claim_slots = table_slots_for(E * static_cast<u64>(P->free_count));
+    const bool use_claims = W == 1 && !(P->flags & 2) && P->hashes == 17 &&
+                            m <= 0xFFFFFFFFull && claim_slots <= kClaimMax;
+    if (m / 32 > B.bloom_cap || (use_claims && claim_slots > B.claim_cap)) {
+        if (gtid == 0) {
+            const bool bloom_short = m / 32 > B.bloom_cap;
+            C->need = bloom_short ? m / 32 : claim_slots;
+            C->abort = bloom_short ? kGrowBloom : kGrowClaims;
+        }
+        return;
+    }
+    // clear the other filter's region from round r-1 (needed clean at r+1)
+    if (r > 0) {
+        const u64 prev_words = bloom_bits_for(round_cap(*P, C->rs[r - 1].expanded), P->bpe) / 32;
+        uint4* w4 = reinterpret_cast<uint4*>(B.bloom[(r + 1) & 1]);
+        const u64 n4 = prev_words / 4;
+        for (u64 i = gtid; i < n4; i += gstride) w4[i] = make_uint4(0, 0, 0, 0);
+        for (u64 i = n4 * 4 + gtid; i < prev_words; i += gstride) B.bloom[(r + 1) & 1][i] = 0;
+    }
+    unsigned* bits = B.bloom[r & 1];
+    load_adjacency<W>(P, adj);
+    __syncthreads();
+    constexpr unsigned kWarpSlots = kWarpLocalBytes / (8 * W);
+    const int lane = threadIdx.x & 31;
+    const int wslot = threadIdx.x & ~31;
+    u64* my_slots = local_slots + (threadIdx.x >> 5) * (kWarpSlots * W);
+    const Set<W> forbidden = param_set<W>(P->forbidden);
+    const bool single_lock = (P->flags & 2) != 0;
+    const u64* in = B.keys[r & 1];
+    const u64 warp = gtid >> 5;
+    const u64 nwarps = gstride >> 5;
+    u64 offered = 0, pruned = 0;
+    for (u64 base = warp * 32; base < E; base += nwarps * 32) {
+        const u64 idx = base + lane;
+        const bool valid = idx < E;
+        const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
+        const Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned)
+                               : Set<W>::zero();
+        offered += M.count();
+        for (unsigned i = lane; i < kWarpSlots * W; i += 32) my_slots[i] = 0;
+#pragma unroll
+        for (int i = 0; i < 2 * W; ++i) novel_words[threadIdx.x][i] = 0;
+        __syncwarp();
+        WarpFlat f;
+        f.scan(M.count());
+        for (int t = 0; t < f.total; t += 32) {
+            const int j = t + lane;
+            const int src = f.source(j);
+            const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
+            const Set<W> Ms = shfl_set<W>(M, src);
+            const Set<W> Ss = shfl_set<W>(S, src);
+            if (j < f.total) {
+                const int v = nth_member<W>(Ms, j - excl);
+                Set<W> key = Ss;
+                key.add(v);
+                bool novel = false;
+                if (local_first<W>(my_slots, kWarpSlots - 1, key)) {
+                    if (use_claims) {
+                        const unsigned h1 = murmur_key<W>(key, kSeed1);
+                        const unsigned h2 = murmur_key<W>(key, kSeed2);
+                        u64 first, step;
+                        probe_start(h1, h2, m, first, step);
+                        novel = bloom_set_bits<17>(bits, m, first, step) &&
+                                claim_key(B.claims, claim_slots - 1, key.w[0], epoch);
+                    } else {
+                        novel = bloom_insert<W>(bits, B.locks, m, P->hashes, key, single_lock);
+                    }
+                }
+                if (novel) atomicOr(&novel_words[wslot + src][v >> 5], 1u << (v & 31));
+            }
+        }
+        __syncwarp();
+        if (valid) {
+            Set<W> nm;
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                nm.w[i] = novel_words[threadIdx.x][2 * i] |
+                          (static_cast<u64>(novel_words[threadIdx.x][2 * i + 1]) << 32);
+            store_set<W>(B.cmask, idx, nm);
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        offered += __shfl_xor_sync(kFull, offered, o);
+        pruned += __shfl_xor_sync(kFull, pruned, o);
+    }
+    if (lane == 0) {
+        if (offered) atomicAdd(&C->rs[r].offered, offered);
+        if (pruned) atomicAdd(&C->rs[r].mmw_pruned, pruned);
+    }
+}
+
+// ----------------------------------------------------------------------
 // K3: ordered append with a single-pass decoupled look-back scan
 // (replaces the cursor append dp.cpp:96-117 and the rank sort + truncation
 // dp.cpp:150-157)
@@ -830,185 +1042,6 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
         }
         __syncthreads();
     }
-    finish_round(P, C, B, r, E, cap);
-}
-
-// ----------------------------------------------------------------------
-// Fused Bloom round (replaces expand_range + the Bloom branch of
-// expand_layer, dp.cpp:39-69 + 93-117): per 256-parent tile
-//   K1 candidates -> block-local exact dedup in shared memory -> global
-//   Bloom insert (fast read-only path, else stripe lock + 17 atomicOr) ->
-//   decoupled look-back scan -> rank-ordered append.
-// Two Bloom filters alternate by round parity; while round r fills filter
-// r&1, its CTAs clear the region round r-1 used in the other filter, so no
-// separate clear pass (or launch) is needed.
-
-constexpr int kLocalBytes = 32 * 1024;  // dynamic shared memory for the tile's key set
-
-// Block-shared open-addressing set of child keys (key 0 = empty: children
-// are never the empty set). Returns true for the first inserter of a key in
-// the tile, and also when the probe budget runs out (the global filter then
-// decides), so a crowded table only costs dedup efficiency, never states.
-template <int W>
-__device__ __forceinline__ bool local_first(u64* slots, unsigned mask, const Set<W>& key) {
-    unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & mask;
-    for (int probe = 0; probe < 32; ++probe) {
-        if constexpr (W == 1) {
-            const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(slots + h), 0ull, key.w[0]);
-            if (prev == 0) return true;
-            if (prev == key.w[0]) return false;
-        } else {
-            u64 lo, hi;
-            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(slots + 2 * h));
-            asm volatile(
-                "{\n\t.reg .b128 c, s, d;\n\t"
-                "mov.b128 c, {%2, %3};\n\t"
-                "mov.b128 s, {%4, %5};\n\t"
-                "atom.shared.cas.b128 d, [%6], c, s;\n\t"
-                "mov.b128 {%0, %1}, d;\n\t}"
-                : "=l"(lo), "=l"(hi)
-                : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
-                : "memory");
-            if ((lo | hi) == 0) return true;
-            if (lo == key.w[0] && hi == key.w[1]) return false;
-        }
-        h = (h + 1) & mask;
-    }
-    return true;
-}
-
-// Position of the child number j of the tile: binary search over the
-// block-inclusive child counts in shared memory (first parent whose
-// inclusive count exceeds j).
-__device__ __forceinline__ int tile_source(const unsigned* incl, unsigned j) {
-    int lo = 0;
-#pragma unroll
-    for (int step = kThreads / 2; step >= 1; step >>= 1)
-        if (incl[lo + step - 1] <= j) lo += step;
-    return lo;
-}
-
-template <int W, bool MMW>
-__global__ void __launch_bounds__(kThreads, 3) k_round_bloom(const Params* __restrict__ P, Control* C,
-                                                             Bufs B) {
-    using BlockScan = cub::BlockScan<unsigned, kThreads>;
-    extern __shared__ __align__(16) u64 local_slots[];
-    __shared__ typename BlockScan::TempStorage scan_tmp;
-    __shared__ Set<W> adj[64 * W];
-    __shared__ Set<W> t_set[kThreads];     // parents of the tile
-    __shared__ Set<W> t_mask[kThreads];    // their candidates, then their novel children
-    __shared__ unsigned t_hist[kThreads];
-    __shared__ unsigned t_incl[kThreads];  // inclusive child counts
-    __shared__ unsigned novel_words[kThreads][2 * W];
-    __shared__ u64 s_prefix;
-    __shared__ u64 s_tile;
-    if (halted(C)) return;
-    const unsigned r = C->round;
-    const unsigned epoch = C->epoch;
-    const u64 E = C->count[r & 1];
-    const u64 cap = round_cap(*P, E);
-    const u64 m = bloom_bits_for(cap, P->bpe);
-    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-    const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
-    if (m / 32 > B.bloom_cap) {
-        if (gtid == 0) {
-            C->need = m / 32;
-            C->abort = kGrowBloom;
-        }
-        return;
-    }
-    // clear the other filter's region from round r-1 (needed clean at r+1)
-    if (r > 0) {
-        const u64 prev_words = bloom_bits_for(round_cap(*P, C->rs[r - 1].expanded), P->bpe) / 32;
-        uint4* w4 = reinterpret_cast<uint4*>(B.bloom[(r + 1) & 1]);
-        const u64 n4 = prev_words / 4;
-        for (u64 i = gtid; i < n4; i += gstride) w4[i] = make_uint4(0, 0, 0, 0);
-        for (u64 i = n4 * 4 + gtid; i < prev_words; i += gstride) B.bloom[(r + 1) & 1][i] = 0;
-    }
-    unsigned* bits = B.bloom[r & 1];
-    load_adjacency<W>(P, adj);
-    const u64 ntiles = (E + kThreads - 1) / kThreads;
-    const u64 limit = cap < B.layer_cap ? cap : B.layer_cap;
-    constexpr unsigned kSlots = kLocalBytes / (8 * W);
-    const Set<W> forbidden = param_set<W>(P->forbidden);
-    const bool single_lock = (P->flags & 2) != 0;
-    const u64* in = B.keys[r & 1];
-    const unsigned* hin = B.hist[r & 1];
-    u64* out = B.keys[(r + 1) & 1];
-    unsigned* hout = B.hist[(r + 1) & 1];
-    u64 offered = 0, pruned = 0;
-
-    for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&C->rs[r].ticket, 1ull);
-        for (unsigned i = threadIdx.x; i < kSlots * W; i += kThreads) local_slots[i] = 0;
-#pragma unroll
-        for (int i = 0; i < 2 * W; ++i) novel_words[threadIdx.x][i] = 0;
-        __syncthreads();
-        const u64 tile = s_tile;
-        if (tile >= ntiles) break;
-        const u64 idx = tile * kThreads + threadIdx.x;
-        const bool valid = idx < E;
-        const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        const Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned)
-                               : Set<W>::zero();
-        t_set[threadIdx.x] = S;
-        t_mask[threadIdx.x] = M;
-        t_hist[threadIdx.x] = valid ? hin[idx] : 0u;
-        unsigned incl, children;
-        BlockScan(scan_tmp).InclusiveSum(static_cast<unsigned>(M.count()), incl, children);
-        t_incl[threadIdx.x] = incl;
-        offered += M.count();
-        __syncthreads();
-        // dedup: children spread evenly over the block (block-level flattening)
-        for (unsigned j = threadIdx.x; j < children; j += kThreads) {
-            const int src = tile_source(t_incl, j);
-            const unsigned before = src ? t_incl[src - 1] : 0u;
-            const int v = nth_member<W>(t_mask[src], static_cast<int>(j - before));
-            Set<W> key = t_set[src];
-            key.add(v);
-            if (local_first<W>(local_slots, kSlots - 1, key) &&
-                bloom_insert<W>(bits, B.locks, m, P->hashes, key, single_lock))
-                atomicOr(&novel_words[src][v >> 5], 1u << (v & 31));
-        }
-        __syncthreads();
-        Set<W> N;
-#pragma unroll
-        for (int i = 0; i < W; ++i)
-            N.w[i] = novel_words[threadIdx.x][2 * i] |
-                     (static_cast<u64>(novel_words[threadIdx.x][2 * i + 1]) << 32);
-        t_mask[threadIdx.x] = N;
-        unsigned nincl, survivors;
-        __syncthreads();  // scan_tmp reuse
-        BlockScan(scan_tmp).InclusiveSum(static_cast<unsigned>(N.count()), nincl, survivors);
-        t_incl[threadIdx.x] = nincl;
-        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, tile, survivors, epoch);
-        __syncthreads();
-        // rank-ordered append, consecutive threads store consecutive states
-        const u64 prefix = s_prefix;
-        for (unsigned j = threadIdx.x; j < survivors; j += kThreads) {
-            const u64 pos = prefix + j;
-            if (pos >= limit) break;  // capacity wall: drop the newest (dp.cpp:107,152-155)
-            const int src = tile_source(t_incl, j);
-            const unsigned before = src ? t_incl[src - 1] : 0u;
-            const int v = nth_member<W>(t_mask[src], static_cast<int>(j - before));
-            Set<W> key = t_set[src];
-            key.add(v);
-            store_set<W>(out, pos, key);
-            hout[pos] = (t_hist[src] << 8) | static_cast<unsigned>(v & 0xFF);  // push_history
-        }
-        if (threadIdx.x == 0 && tile == ntiles - 1) C->rs[r].unique = prefix + survivors;
-        __syncthreads();
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        offered += __shfl_xor_sync(kFull, offered, o);
-        pruned += __shfl_xor_sync(kFull, pruned, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (offered) atomicAdd(&C->rs[r].offered, offered);
-        if (pruned) atomicAdd(&C->rs[r].mmw_pruned, pruned);
-    }
-    __syncthreads();
     finish_round(P, C, B, r, E, cap);
 }
 
@@ -1219,10 +1252,7 @@ private:
         epoch_ = (epoch_ + 1) & kEpochMask;
         if (epoch_ == 0) {
             epoch_ = 1;
-            if (b_.tiles)
-                check(cudaMemsetAsync(b_.tiles, 0, ((b_.layer_cap + kThreads - 1) / kThreads + 1) * 8,
-                                      stream_),
-                      "tiles clear");
+            clear_tagged();
         }
         return epoch_;
     }
@@ -1259,12 +1289,12 @@ private:
             check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLocalBytes),
                   "smem attribute");
         };
-        allow(k_round_bloom<1, false>);
-        allow(k_round_bloom<1, true>);
-        allow(k_round_bloom<2, false>);
-        allow(k_round_bloom<2, true>);
+        allow(k_bloom_dedup<1, false>);
+        allow(k_bloom_dedup<1, true>);
+        allow(k_bloom_dedup<2, false>);
+        allow(k_bloom_dedup<2, true>);
         int per_sm = 0;
-        check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_round_bloom<1, false>, kThreads,
+        check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bloom_dedup<1, false>, kThreads,
                                                             kLocalBytes),
               "occupancy");
         grid_fused_ = prop.multiProcessorCount * std::max(1, per_sm);
@@ -1386,6 +1416,25 @@ private:
         }
     }
 
+    // Claim slots are {key, epoch}; fresh memory is zero (epoch 0 is never a
+    // live tag), and a look-back epoch wrap clears the table again.
+    void ensure_claims(u64 slots) {
+        if (slots <= b_.claim_cap && b_.claims) return;
+        const u64 cap = std::max<u64>(slots, u64{1} << 20);
+        if (b_.claims) cudaFree(b_.claims);
+        check(cudaMalloc(&b_.claims, cap * 16), "claims");
+        check(cudaMemsetAsync(b_.claims, 0, cap * 16, stream_), "claims zero");
+        b_.claim_cap = cap;
+    }
+
+    // Epoch-tagged structures (look-back statuses, claim slots) after a wrap.
+    void clear_tagged() {
+        if (b_.tiles)
+            check(cudaMemsetAsync(b_.tiles, 0, ((b_.layer_cap + kThreads - 1) / kThreads + 1) * 8, stream_),
+                  "tiles clear");
+        if (b_.claims) check(cudaMemsetAsync(b_.claims, 0, b_.claim_cap * 16, stream_), "claims clear");
+    }
+
     u64 host_round_cap(u64 e_in) const {
         u64 upper = e_in * static_cast<u64>(h_params_->free_count);
         if (upper < 1) upper = 1;
@@ -1434,11 +1483,13 @@ private:
         };
         if (!exact) {
             if (cfg.use_mmw)
-                timed_launch([&] { k_round_bloom<W, true><<<grid_fused_, kThreads, kLocalBytes, stream_>>>(d_params_, d_ctl_, b_); },
-                             prof.t.fused_ms, prof.t.fused_launches);
+                timed_launch([&] { k_bloom_dedup<W, true><<<grid_fused_, kThreads, kLocalBytes, stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.insert_ms, prof.t.insert_launches);
             else
-                timed_launch([&] { k_round_bloom<W, false><<<grid_fused_, kThreads, kLocalBytes, stream_>>>(d_params_, d_ctl_, b_); },
-                             prof.t.fused_ms, prof.t.fused_launches);
+                timed_launch([&] { k_bloom_dedup<W, false><<<grid_fused_, kThreads, kLocalBytes, stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.insert_ms, prof.t.insert_launches);
+            timed_launch([&] { k_append<W, false><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
+                         prof.t.append_ms, prof.t.append_launches);
             return;
         }
         if (cfg.use_mmw)
@@ -1460,10 +1511,7 @@ private:
         // from there (a wrap past 2^24 clears the status array)
         if (h_ctl_->epoch < epoch_) {
             epoch_ = h_ctl_->epoch;
-            if (b_.tiles)
-                check(cudaMemsetAsync(b_.tiles, 0, ((b_.layer_cap + kThreads - 1) / kThreads + 1) * 8,
-                                      stream_),
-                      "tiles clear");
+            clear_tagged();
         } else {
             epoch_ = h_ctl_->epoch;
         }
@@ -1472,6 +1520,7 @@ private:
     void run_rounds(int W, const DpConfig& cfg, int rounds, int k, const LayerObserver* observer) {
         ensure_table(u64{1} << 20);
         ensure_bloom(u64{1} << 22);
+        ensure_claims(u64{1} << 20);
         bloom_round_ = cfg.dedup == DedupMode::bloom;
         if (bloom_round_) clean_blooms();
         if (!prof.on) check(cudaEventRecord(ev_[0], stream_), "event");
@@ -1548,6 +1597,9 @@ private:
                 break;
             case kGrowBloom:
                 ensure_bloom(c.need + c.need / 4);
+                break;
+            case kGrowClaims:
+                ensure_claims(c.need);
                 break;
             default:
                 throw DeviceError("device engine: unknown abort code");
