@@ -719,8 +719,12 @@ __device__ __forceinline__ bool claim_key(u64* claims, u64 mask, u64 key, u64 ta
     u64 i = fmix64(key ^ 0x9E3779B97F4A7C15ULL) & mask;
     for (;;) {
         u64* slot = claims + 2 * i;
-        u64 lo, hi;
-        cas128(slot, ~u64{0}, ~u64{0}, ~u64{0}, ~u64{0}, lo, hi);  // untorn read
+        // A plain 16-byte load may tear, so it only seeds the CAS: a stale
+        // tag goes straight to the claiming CAS (which fails on any tear and
+        // returns the true value); a live tag is re-read untorn first.
+        const ulonglong2 seen = __ldcg(reinterpret_cast<const ulonglong2*>(slot));
+        u64 lo = seen.x, hi = seen.y;
+        if (hi == tag) cas128(slot, ~u64{0}, ~u64{0}, ~u64{0}, ~u64{0}, lo, hi);
         for (;;) {
             if (hi == tag) {
                 if (lo == key) return false;
