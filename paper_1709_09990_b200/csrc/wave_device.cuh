@@ -1,0 +1,745 @@
+// Device building blocks shared by the single-device engine (wavefront.cu)
+// and the owner-sharded engine (shard.cu): vertex-set access, the Q(S,v)
+// candidate test (graph.hpp:61-78 / dp.cpp:39-69), Murmur3 + Bloom probes
+// (bloom.cpp:27-97), the exact open-addressing table (dp.cpp:118-151
+// semantics) and the decoupled look-back scan used by every ordered append.
+// Everything lives in an anonymous namespace: each .cu is its own device
+// translation unit (no -rdc).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "mmw.hpp"
+#include "vset.hpp"
+
+namespace etw {
+namespace {
+constexpr int kThreads = 256;
+constexpr int kMaxRounds = 130;
+constexpr unsigned kFull = 0xffffffffu;
+// Bloom stripe locks. The reference uses 65,536 mutex stripes keyed by
+// h1 (bloom.cpp:18-23); any key -> stripe map keeps inserts of one key
+// serialised, and ~10^5 concurrent device threads need more stripes to keep
+// unrelated keys from contending.
+constexpr int kStripes = 1 << 20;
+constexpr unsigned kSeed1 = 0x9747B28Cu;  // bloom.hpp:24
+constexpr unsigned kSeed2 = 0x5EEDBA5Eu;  // bloom.hpp:25
+
+using u64 = unsigned long long;
+
+struct Params {
+    int n, k, rounds, free_count;
+    int hashes, bpe, any_pop, flags;  // flags: ETWG_DEBUG bits (tests only)
+    u64 max_states;
+    u64 forbidden[2];
+    u64 rows[kMaxVertices][2];
+};
+
+// ----------------------------------------------------------------------
+// small device helpers
+
+template <int W>
+__device__ __forceinline__ Set<W> load_set(const u64* p, u64 i) {
+    Set<W> s;
+    if constexpr (W == 1) {
+        s.w[0] = p[i];
+    } else {
+        ulonglong2 v = reinterpret_cast<const ulonglong2*>(p)[i];
+        s.w[0] = v.x;
+        s.w[1] = v.y;
+    }
+    return s;
+}
+
+template <int W>
+__device__ __forceinline__ void store_set(u64* p, u64 i, const Set<W>& s) {
+    if constexpr (W == 1) {
+        p[i] = s.w[0];
+    } else {
+        reinterpret_cast<ulonglong2*>(p)[i] = make_ulonglong2(s.w[0], s.w[1]);
+    }
+}
+
+template <int W>
+__device__ __forceinline__ Set<W> shfl_set(const Set<W>& s, int src) {
+    Set<W> r;
+#pragma unroll
+    for (int i = 0; i < W; ++i) r.w[i] = __shfl_sync(kFull, s.w[i], src);
+    return r;
+}
+
+// position of the r-th (0-based) set bit of x; requires popc(x) > r
+__device__ __forceinline__ int nth_bit64(u64 x, int r) {
+    int pos = 0;
+#pragma unroll
+    for (int w = 32; w >= 1; w >>= 1) {
+        u64 low = x & ((u64{1} << w) - 1);
+        int c = __popcll(low);
+        if (r >= c) {
+            r -= c;
+            x >>= w;
+            pos += w;
+        }
+    }
+    return pos;
+}
+
+template <int W>
+__device__ __forceinline__ int nth_member(const Set<W>& s, int r) {
+    if constexpr (W == 1) {
+        return nth_bit64(s.w[0], r);
+    } else {
+        int c0 = __popcll(s.w[0]);
+        return r < c0 ? nth_bit64(s.w[0], r) : 64 + nth_bit64(s.w[1], r - c0);
+    }
+}
+
+// Warp-wide flattening of per-lane child masks: after scan(), iteration t
+// hands lane l the child number t*32+l in (lane, vertex) order.
+struct WarpFlat {
+    int cnt, incl, total;
+    __device__ __forceinline__ void scan(int c) {
+        const int lane = threadIdx.x & 31;
+        cnt = c;
+        incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+        }
+        total = __shfl_sync(kFull, incl, 31);
+    }
+    // lane holding child j (warp-uniform control flow required)
+    __device__ __forceinline__ int source(int j) const {
+        int src = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            int c = __shfl_sync(kFull, incl, src + step - 1);
+            if (c <= j) src += step;
+        }
+        return src > 31 ? 31 : src;
+    }
+};
+
+__device__ __forceinline__ u64 fmix64(u64 k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdULL;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ULL;
+    k ^= k >> 33;
+    return k;
+}
+
+template <int W>
+__device__ __forceinline__ u64 slot_hash(const Set<W>& s) {
+    u64 h = fmix64(s.w[0]);
+    if constexpr (W == 2) h = fmix64(h ^ (s.w[1] + 0x9E3779B97F4A7C15ULL));
+    return h;
+}
+
+// Murmur3 x86_32 over the little-endian bytes of the key (bloom.cpp:27-64):
+// 8 bytes for n <= 64 (the reference key, bloom.cpp:66-70), 16 for n <= 128.
+__device__ __forceinline__ unsigned rotl32(unsigned x, int r) { return __funnelshift_l(x, x, r); }
+
+template <int W>
+__device__ __forceinline__ unsigned murmur_key(const Set<W>& key, unsigned seed) {
+    unsigned h = seed;
+#pragma unroll
+    for (int i = 0; i < 2 * W; ++i) {
+        unsigned k = static_cast<unsigned>(key.w[i >> 1] >> (32 * (i & 1)));
+        k *= 0xcc9e2d51u;
+        k = rotl32(k, 15);
+        k *= 0x1b873593u;
+        h ^= k;
+        h = rotl32(h, 13);
+        h = h * 5 + 0xe6546b64u;
+    }
+    h ^= 8u * W;
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+
+__host__ __device__ __forceinline__ u64 bloom_bits_for(u64 expected, int bpe) {
+    u64 bits = expected * static_cast<u64>(bpe);
+    u64 m = (bits + 63) / 64 * 64;  // bloom.cpp:74-75
+    return m < 64 ? 64 : m;
+}
+
+__host__ __device__ __forceinline__ u64 round_cap(const Params& p, u64 e_in) {
+    u64 upper = e_in * static_cast<u64>(p.free_count);  // dp.cpp:84-86
+    if (upper < 1) upper = 1;
+    return p.max_states < upper ? p.max_states : upper;
+}
+
+__host__ __device__ __forceinline__ u64 table_slots_for(u64 offered) {
+    u64 want = 2 * offered + 1024;
+    u64 s = 1024;
+    while (s < want) s <<= 1;
+    return s;
+}
+
+template <int W>
+__device__ __forceinline__ Set<W> param_set(const u64 (&w)[2]) {
+    Set<W> s;
+#pragma unroll
+    for (int i = 0; i < W; ++i) s.w[i] = w[i];
+    return s;
+}
+
+// ----------------------------------------------------------------------
+// K1: candidate evaluation (replaces expand_range + q_set, dp.cpp:39-69,
+// graph.hpp:61-78, and the MMW prune driven at dp.cpp:51-63)
+
+// For every u in S: R[u] = N(K_u) \ S, the outside boundary of u's component
+// K_u of G[S] (flood fill over bitmask rows, one pass per component).
+template <int W>
+__device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>& S, Set<W>* R) {
+    Set<W> rem = S;
+    while (rem.any()) {
+        Set<W> comp = Set<W>::bit(rem.lowest());
+        Set<W> frontier = comp;
+        Set<W> nb = Set<W>::zero();
+        while (frontier.any()) {
+            const Set<W> a = adj[frontier.pop()];
+            nb |= a;
+            Set<W> fresh = (a & S) - comp;
+            comp |= fresh;
+            frontier |= fresh;
+        }
+        rem = rem - comp;
+        const Set<W> boundary = nb - S;
+        for (int u : members(comp)) R[u] = boundary;
+    }
+}
+
+// Q(S,v) (graph.hpp:61-78): v's own outside neighbours plus the boundary of
+// every component of G[S] that v touches, i.e. of K_u for u in N(v) & S.
+// Costs |N(v) & S| mask ORs instead of a DFS per (S, v).
+template <int W>
+__device__ __forceinline__ Set<W> reach_from(const Set<W>* adj, const Set<W>& S, const Set<W>* R,
+                                             int v) {
+    Set<W> q = adj[v] - S;
+    for (int u : members(adj[v] & S)) q |= R[u];
+    q.del(v);
+    return q;
+}
+
+// Minor-min-width on eliminate(G, S + v) (init_view_after, mmw.cpp:20-43,
+// then the shared contraction loop of mmw.hpp). rows[w] = Q(S,w) for every
+// w outside S. Returns early once the bound exceeds cap.
+template <int W>
+__device__ int mmw_child(const Set<W>* adj, int n, int cap, const Set<W>& S, int v,
+                         const Set<W>* rows) {
+    constexpr int N = 64 * W;
+    unsigned char parent[N];
+    unsigned char degree[N];
+    MinorState<W> m{adj, S, Set<W>::zero(), parent, degree};
+    m.elim.add(v);
+    m.alive = Set<W>::prefix(n) - m.elim;
+    for (int x = 0; x < n; ++x) {
+        parent[x] = static_cast<unsigned char>(x);
+        degree[x] = 0;
+    }
+    // eliminating v turns Q(S,v) into a clique; everyone else keeps Q(S,w)
+    for (int w : members(m.alive)) {
+        if (rows[v].has(w)) {
+            Set<W> j = rows[w] | rows[v];
+            j.del(v);
+            j.del(w);
+            degree[w] = static_cast<unsigned char>(j.count());
+        } else {
+            degree[w] = static_cast<unsigned char>(rows[w].count());
+        }
+    }
+    return minor_min_width<W>(m, cap);
+}
+
+template <int W, bool MMW>
+__device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, const Set<W>& S,
+                                             const Set<W>& forbidden, u64& pruned) {
+    constexpr int N = 64 * W;
+    const Set<W> open = Set<W>::prefix(n) - S;
+    const Set<W> eligible = open - forbidden;
+    Set<W> keep = Set<W>::zero();
+    if (eligible.none()) return keep;
+    Set<W> R[N];
+    component_reach<W>(adj, S, R);
+    if constexpr (!MMW) {
+        for (int v : members(eligible))
+            if (reach_from<W>(adj, S, R, v).count() <= k) keep.add(v);
+    } else {
+        Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
+        for (int w : members(open)) rows[w] = reach_from<W>(adj, S, R, w);
+        for (int v : members(eligible)) {
+            if (rows[v].count() > k) continue;
+            if (mmw_child<W>(adj, n, k, S, v, rows) > k) {
+                ++pruned;
+                continue;
+            }
+            keep.add(v);
+        }
+    }
+    return keep;
+}
+
+template <int W>
+__device__ __forceinline__ void load_adjacency(const Params* P, Set<W>* adj) {
+    for (int i = threadIdx.x; i < P->n; i += blockDim.x) adj[i] = param_set<W>(P->rows[i]);
+}
+
+// ----------------------------------------------------------------------
+// K2a: exact dedup — open addressing, claim by CAS, keep min emission rank
+// (replaces the exact branch's sort/unique, dp.cpp:118-151)
+
+// Rank words carry a round tag in bits 48..63 that shrinks as rounds
+// advance, so any stale rank left by an earlier round of this decide loses
+// every atomicMin; keys of a round all have popcount round+1, so stale keys
+// are recognised without clearing the table between rounds.
+__device__ __forceinline__ u64 rank_tag(unsigned r) { return static_cast<u64>(kMaxRounds - r) << 48; }
+
+template <int W>
+__device__ __forceinline__ bool stale_key(const Set<W>& cur, int want_pop) {
+    return want_pop < 0 ? cur.none() : cur.count() != want_pop;
+}
+
+__device__ __forceinline__ void cas128(u64* addr, u64 exp_lo, u64 exp_hi, u64 new_lo, u64 new_hi,
+                                       u64& old_lo, u64& old_hi) {
+    asm volatile(
+        "{\n\t.reg .b128 c, s, d;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 s, {%4, %5};\n\t"
+        "atom.global.cas.b128 d, [%6], c, s;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(old_lo), "=l"(old_hi)
+        : "l"(exp_lo), "l"(exp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
+        : "memory");
+}
+
+// Slot layout: W=1 {key, rank}; W=2 {key.lo, key.hi, rank, pad}.
+template <int W>
+__device__ __forceinline__ u64* table_slot(u64* table, u64 i) {
+    return table + i * (W == 1 ? 2 : 4);
+}
+
+// Inserts `key` with `rank` (kept as the minimum of all inserts of the key).
+// Returns 1 when this call claimed a fresh slot for the key, 0 when the key
+// was present, -1 when `max_probes` slots were probed without finding a
+// place (the table is over-full: the caller aborts the round and grows it).
+constexpr int kMaxProbes = 1 << 12;
+
+template <int W>
+__device__ int table_insert(u64* table, u64 mask, int want_pop, const Set<W>& key, u64 rank,
+                            int max_probes = kMaxProbes) {
+    u64 i = slot_hash<W>(key) & mask;
+    for (int probe = 0; probe < max_probes; ++probe) {
+        u64* slot = table_slot<W>(table, i);
+        int fresh = 0;
+        if constexpr (W == 1) {
+            u64 cur = *reinterpret_cast<volatile u64*>(slot);
+            for (;;) {
+                if (cur == key.w[0]) break;
+                Set<1> c;
+                c.w[0] = cur;
+                if (!stale_key<1>(c, want_pop)) break;
+                u64 prev = atomicCAS(slot, cur, key.w[0]);
+                if (prev == cur) {
+                    cur = key.w[0];
+                    fresh = 1;
+                    break;
+                }
+                cur = prev;
+            }
+            if (cur == key.w[0]) {
+                atomicMin(slot + 1, rank);
+                return fresh;
+            }
+        } else {
+            // 128-bit keys: read through a failing CAS so the view is never torn
+            u64 lo, hi;
+            cas128(slot, ~u64{0}, ~u64{0}, ~u64{0}, ~u64{0}, lo, hi);
+            for (;;) {
+                if (lo == key.w[0] && hi == key.w[1]) break;
+                Set<2> c;
+                c.w[0] = lo;
+                c.w[1] = hi;
+                if (!stale_key<2>(c, want_pop)) break;
+                u64 plo, phi;
+                cas128(slot, lo, hi, key.w[0], key.w[1], plo, phi);
+                if (plo == lo && phi == hi) {
+                    lo = key.w[0];
+                    hi = key.w[1];
+                    fresh = 1;
+                    break;
+                }
+                lo = plo;
+                hi = phi;
+            }
+            if (lo == key.w[0] && hi == key.w[1]) {
+                atomicMin(slot + 2, rank);
+                return fresh;
+            }
+        }
+        i = (i + 1) & mask;
+    }
+    return -1;
+}
+
+// After all inserts of the round: the rank stored with `key`.
+template <int W>
+__device__ __forceinline__ u64 table_rank(const u64* table, u64 mask, const Set<W>& key) {
+    u64 i = slot_hash<W>(key) & mask;
+    for (;;) {
+        const u64* slot = table + i * (W == 1 ? 2 : 4);
+        bool hit = slot[0] == key.w[0];
+        if constexpr (W == 2) hit = hit && slot[1] == key.w[1];
+        if (hit) return slot[W == 1 ? 1 : 2];
+        i = (i + 1) & mask;
+    }
+}
+
+template <int W>
+__device__ __forceinline__ u64 child_rank(u64 parent_idx, int v) {
+    return parent_idx * (64 * W) + static_cast<u64>(v);  // dp.cpp:66 (idx*64+v)
+}
+
+// ----------------------------------------------------------------------
+// CTA-scope duplicate filter. A tile of consecutive parents (siblings of the
+// same grandparents sit next to each other in a rank-ordered layer) offers
+// many identical children; resolving them in shared memory first means only
+// one instance per key and tile goes on to the global table / filter / owner
+// (the one with the smallest emission rank, so min-rank semantics survive).
+template <int W, int SLOTS>
+struct TileSet {
+    u64 keys[SLOTS * W];  // 0 = empty (children are never the empty set)
+    unsigned rank[SLOTS];
+};
+
+template <int W, int SLOTS>
+__device__ __forceinline__ void tile_set_clear(TileSet<W, SLOTS>& t) {
+    for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) t.keys[i] = 0;
+    for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) t.rank[i] = 0xffffffffu;
+}
+
+constexpr int kTileProbes = 32;
+
+// Inserts (key, rank); a key whose probe window is full stays out of the set
+// for good (slots are never freed), so every instance of it reads as a
+// winner in tile_set_winner and goes on to the global structure.
+template <int W, int SLOTS>
+__device__ __forceinline__ void tile_set_insert(TileSet<W, SLOTS>& t, const Set<W>& key, unsigned rank) {
+    unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
+    for (int probe = 0; probe < kTileProbes; ++probe) {
+        if constexpr (W == 1) {
+            const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(&t.keys[h]), 0ull, key.w[0]);
+            if (prev == 0 || prev == key.w[0]) {
+                atomicMin(&t.rank[h], rank);
+                return;
+            }
+        } else {
+            u64 lo, hi;
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&t.keys[2 * h]));
+            asm volatile(
+                "{\n\t.reg .b128 c, s, d;\n\t"
+                "mov.b128 c, {%2, %3};\n\t"
+                "mov.b128 s, {%4, %5};\n\t"
+                "atom.shared.cas.b128 d, [%6], c, s;\n\t"
+                "mov.b128 {%0, %1}, d;\n\t}"
+                : "=l"(lo), "=l"(hi)
+                : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
+                : "memory");
+            if ((lo | hi) == 0 || (lo == key.w[0] && hi == key.w[1])) {
+                atomicMin(&t.rank[h], rank);
+                return;
+            }
+        }
+        h = (h + 1) & (SLOTS - 1);
+    }
+}
+
+// After every insert of the tile: true iff `rank` is the key's tile minimum
+// (or the key never found room).
+template <int W, int SLOTS>
+__device__ __forceinline__ bool tile_set_winner(const TileSet<W, SLOTS>& t, const Set<W>& key,
+                                                unsigned rank) {
+    unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
+    for (int probe = 0; probe < kTileProbes; ++probe) {
+        bool hit = t.keys[W * h] == key.w[0];
+        if constexpr (W == 2) hit = hit && t.keys[2 * h + 1] == key.w[1];
+        if (hit) return t.rank[h] == rank;
+        h = (h + 1) & (SLOTS - 1);
+    }
+    return true;
+}
+
+// Replaces each thread's child mask M (children S+v) by the mask of its
+// tile winners. Call with all threads of the CTA; t must be clear on entry
+// and `win` is a per-thread scratch row of 2W words.
+template <int W, int SLOTS>
+__device__ __forceinline__ void tile_dedup(TileSet<W, SLOTS>& t, unsigned (*win)[2 * W], const Set<W>& S,
+                                           Set<W>& M) {
+    const int lane = threadIdx.x & 31;
+    const int wslot = threadIdx.x & ~31;
+    WarpFlat f;
+    f.scan(M.count());
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+#pragma unroll
+            for (int i = 0; i < 2 * W; ++i) win[threadIdx.x][i] = 0;
+            __syncthreads();  // every insert of the tile is done
+        }
+        for (int tt = 0; tt < f.total; tt += 32) {
+            const int j = tt + lane;
+            const int src = f.source(j);
+            const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
+            const Set<W> Ms = shfl_set<W>(M, src);
+            const Set<W> Ss = shfl_set<W>(S, src);
+            if (j < f.total) {
+                const int v = nth_member<W>(Ms, j - excl);
+                Set<W> key = Ss;
+                key.add(v);
+                const unsigned rank = static_cast<unsigned>(wslot + src) * (64 * W) + v;
+                if (pass == 0)
+                    tile_set_insert<W, SLOTS>(t, key, rank);
+                else if (tile_set_winner<W, SLOTS>(t, key, rank))
+                    atomicOr(&win[wslot + src][v >> 5], 1u << (v & 31));
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < W; ++i)
+        M.w[i] = win[threadIdx.x][2 * i] | (static_cast<u64>(win[threadIdx.x][2 * i + 1]) << 32);
+}
+
+// ----------------------------------------------------------------------
+// K2b: Bloom dedup on the reference's bit positions (bloom.cpp:86-97)
+
+// Stripe lock with acquire / release semantics (no full fences): the 17
+// relaxed atomicOr of a locked insert stay between the two.
+__device__ __forceinline__ void stripe_lock(unsigned* lock) {
+    unsigned old;
+    for (;;) {
+        asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "l"(lock) : "memory");
+        if (old == 0) return;
+        __nanosleep(64);
+    }
+}
+
+__device__ __forceinline__ void stripe_unlock(unsigned* lock) {
+    asm volatile("st.release.gpu.global.b32 [%0], 0;" ::"l"(lock) : "memory");
+}
+
+// Probe positions (h1 + i*h2) mod m, i = 1..hashes (bloom.cpp:90-91),
+// stepped incrementally: pos_{i+1} = pos_i + (h2 mod m) - [>= m]*m.
+__device__ __forceinline__ void probe_start(unsigned h1, unsigned h2, u64 m, u64& first, u64& step) {
+    if (m <= 0xFFFFFFFFull) {  // 32-bit division whenever m fits
+        const unsigned m32 = static_cast<unsigned>(m);
+        const unsigned s = h2 % m32;
+        const u64 f = static_cast<u64>(h1 % m32) + s;
+        step = s;
+        first = f >= m ? f - m : f;
+    } else {
+        step = static_cast<u64>(h2) % m;
+        first = (static_cast<u64>(h1) + static_cast<u64>(h2)) % m;
+    }
+}
+
+// insert_and_check (bloom.cpp:86-97) on the device. H > 0 fixes the hash
+// count at compile time so all probe loads / atomics are issued back to
+// back; H == 0 is the generic runtime-count loop.
+template <int W, int H>
+__device__ __forceinline__ bool bloom_insert_h(unsigned* bits, unsigned* locks, u64 m, int hashes,
+                                               const Set<W>& key, bool single_lock) {
+    const unsigned h1 = murmur_key<W>(key, kSeed1);
+    const unsigned h2 = murmur_key<W>(key, kSeed2);
+    u64 first, step;
+    probe_start(h1, h2, m, first, step);
+    // Fast path without the lock: when every probe bit is already set the
+    // key is a duplicate in any serialisation of the concurrent inserts
+    // (most children are: duplicates outnumber novel states ~6:1), so only
+    // inserts that can still be novel pay for the stripe lock and atomics.
+    bool all_set = true;
+    if constexpr (H > 0) {  // requires m < 2^32: positions fit 32 bits
+        unsigned pos[H];
+        unsigned word[H];
+        const unsigned m32 = static_cast<unsigned>(m), step32 = static_cast<unsigned>(step);
+        pos[0] = static_cast<unsigned>(first);
+#pragma unroll
+        for (int i = 1; i < H; ++i) {
+            const unsigned p = pos[i - 1] + step32;  // < 2m: wraps past 2^32 only if m > 2^31
+            pos[i] = (p >= m32 || p < pos[i - 1]) ? p - m32 : p;
+        }
+#pragma unroll
+        for (int i = 0; i < H; ++i) word[i] = __ldcg(bits + (pos[i] >> 5));
+#pragma unroll
+        for (int i = 0; i < H; ++i) all_set &= ((word[i] >> (pos[i] & 31)) & 1u) != 0;
+        if (all_set) return false;
+        unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
+        stripe_lock(lock);
+#pragma unroll
+        for (int i = 0; i < H; ++i) word[i] = atomicOr(bits + (pos[i] >> 5), 1u << (pos[i] & 31));
+        stripe_unlock(lock);
+        bool novel = false;
+#pragma unroll
+        for (int i = 0; i < H; ++i) novel |= ((word[i] >> (pos[i] & 31)) & 1u) == 0;
+        return novel;
+    } else {
+        u64 pos = first;
+        for (int i = 1; i <= hashes; ++i) {
+            const unsigned word = __ldcg(bits + (pos >> 5));
+            all_set &= ((word >> (pos & 31)) & 1u) != 0;
+            pos += step;
+            if (pos >= m) pos -= m;
+        }
+        if (all_set) return false;
+        pos = first;
+        unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
+        stripe_lock(lock);
+        bool novel = false;
+        for (int i = 1; i <= hashes; ++i) {
+            const unsigned bit = 1u << (pos & 31);
+            const unsigned old = atomicOr(bits + (pos >> 5), bit);
+            novel |= (old & bit) == 0;
+            pos += step;
+            if (pos >= m) pos -= m;
+        }
+        stripe_unlock(lock);
+        return novel;
+    }
+}
+
+template <int W>
+__device__ __forceinline__ bool bloom_insert(unsigned* bits, unsigned* locks, u64 m, int hashes,
+                                             const Set<W>& key, bool single_lock = false) {
+    return hashes == 17 && m <= 0xFFFFFFFFull
+               ? bloom_insert_h<W, 17>(bits, locks, m, hashes, key, single_lock)
+               : bloom_insert_h<W, 0>(bits, locks, m, hashes, key, single_lock);
+}
+
+constexpr int kWarpLocalBytes = 4096;               // per-warp key set
+constexpr int kLocalBytes = kWarpLocalBytes * (kThreads / 32);
+constexpr u64 kClaimMax = u64{1} << 27;             // slots (16 B each)
+
+// Warp-private open-addressing set (key 0 = empty; children are never the
+// empty set). True for the first inserter, and when the probe budget runs
+// out (the global filter then decides: costs dedup efficiency, never states).
+template <int W>
+__device__ __forceinline__ bool local_first(u64* slots, unsigned mask, const Set<W>& key) {
+    unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & mask;
+    for (int probe = 0; probe < 16; ++probe) {
+        if constexpr (W == 1) {
+            const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(slots + h), 0ull, key.w[0]);
+            if (prev == 0) return true;
+            if (prev == key.w[0]) return false;
+        } else {
+            u64 lo, hi;
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(slots + 2 * h));
+            asm volatile(
+                "{\n\t.reg .b128 c, s, d;\n\t"
+                "mov.b128 c, {%2, %3};\n\t"
+                "mov.b128 s, {%4, %5};\n\t"
+                "atom.shared.cas.b128 d, [%6], c, s;\n\t"
+                "mov.b128 {%0, %1}, d;\n\t}"
+                : "=l"(lo), "=l"(hi)
+                : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
+                : "memory");
+            if ((lo | hi) == 0) return true;
+            if (lo == key.w[0] && hi == key.w[1]) return false;
+        }
+        h = (h + 1) & mask;
+    }
+    return true;
+}
+
+// Claims a 64-bit key for this round attempt (tag = epoch) in the
+// open-addressing claim table; true iff this call is the first claim.
+__device__ __forceinline__ bool claim_key(u64* claims, u64 mask, u64 key, u64 tag) {
+    u64 i = fmix64(key ^ 0x9E3779B97F4A7C15ULL) & mask;
+    for (;;) {
+        u64* slot = claims + 2 * i;
+        // A plain 16-byte load may tear, so it only seeds the CAS: a stale
+        // tag goes straight to the claiming CAS (which fails on any tear and
+        // returns the true value); a live tag is re-read untorn first.
+        const ulonglong2 seen = __ldcg(reinterpret_cast<const ulonglong2*>(slot));
+        u64 lo = seen.x, hi = seen.y;
+        if (hi == tag) cas128(slot, ~u64{0}, ~u64{0}, ~u64{0}, ~u64{0}, lo, hi);
+        for (;;) {
+            if (hi == tag) {
+                if (lo == key) return false;
+                break;  // another key of this round: probe on
+            }
+            u64 plo, phi;
+            cas128(slot, lo, hi, key, tag, plo, phi);
+            if (plo == lo && phi == hi) return true;
+            lo = plo;
+            hi = phi;
+        }
+        i = (i + 1) & mask;
+    }
+}
+
+// Sets the key's probe bits (relaxed atomicOr); true when one was clear.
+template <int H>
+__device__ __forceinline__ bool bloom_set_bits(unsigned* bits, u64 m, u64 first, u64 step) {
+    unsigned pos[H];
+    unsigned word[H];
+    const unsigned m32 = static_cast<unsigned>(m), step32 = static_cast<unsigned>(step);
+    pos[0] = static_cast<unsigned>(first);
+#pragma unroll
+    for (int i = 1; i < H; ++i) {
+        const unsigned p = pos[i - 1] + step32;
+        pos[i] = (p >= m32 || p < pos[i - 1]) ? p - m32 : p;
+    }
+#pragma unroll
+    for (int i = 0; i < H; ++i) word[i] = __ldcg(bits + (pos[i] >> 5));
+    bool all_set = true;
+#pragma unroll
+    for (int i = 0; i < H; ++i) all_set &= ((word[i] >> (pos[i] & 31)) & 1u) != 0;
+    if (all_set) return false;  // duplicate (or false positive) in any serialisation
+#pragma unroll
+    for (int i = 0; i < H; ++i) word[i] = atomicOr(bits + (pos[i] >> 5), 1u << (pos[i] & 31));
+    bool any_clear = false;
+#pragma unroll
+    for (int i = 0; i < H; ++i) any_clear |= ((word[i] >> (pos[i] & 31)) & 1u) == 0;
+    return any_clear;
+}
+
+// Tile status word: [epoch:24][flag:2][value:38]. The epoch changes with
+// every round attempt, so statuses left by earlier rounds read as "not yet
+// published" and the status array never needs clearing between rounds.
+constexpr u64 kFlagAgg = u64{1} << 38;
+constexpr u64 kFlagPre = u64{2} << 38;
+constexpr u64 kValMask = (u64{1} << 38) - 1;
+constexpr unsigned kEpochMask = (1u << 24) - 1;
+
+__device__ __forceinline__ u64 look_back(u64* tiles, u64 tile, u64 total, unsigned epoch) {
+    volatile u64* vt = tiles;
+    const u64 tag = static_cast<u64>(epoch & kEpochMask) << 40;
+    if (tile == 0) {
+        vt[0] = tag | kFlagPre | total;
+        return 0;
+    }
+    vt[tile] = tag | kFlagAgg | total;
+    u64 prefix = 0;
+    u64 t = tile - 1;
+    for (;;) {
+        const u64 s = vt[t];
+        if ((s >> 40) != (tag >> 40) || (s & (kFlagAgg | kFlagPre)) == 0) {
+            __nanosleep(20);
+            continue;
+        }
+        prefix += s & kValMask;
+        if (s & kFlagPre) break;
+        --t;
+    }
+    __threadfence();
+    vt[tile] = tag | kFlagPre | (prefix + total);
+    return prefix;
+}
+
+}  // namespace
+}  // namespace etw

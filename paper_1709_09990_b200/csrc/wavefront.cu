@@ -5,20 +5,22 @@
 //
 // Per round (one BFS layer of the Held-Karp prefix DP) the device runs:
 //   bloom : k_bloom_dedup -> k_append<mask>
-//   exact : k_expand -> k_exact_insert -> k_append<probe>
+//   exact : k_exact_scatter -> k_exact_part -> k_append
 //
-//   k_expand       one thread per parent S. The components of G[S] are
+//   candidates     one thread per parent S. The components of G[S] are
 //                  flood-filled once with bitmask ops; Q(S,v) for every
 //                  candidate is then the union of v's outside neighbours and
-//                  the outside boundary of every component v touches. The
-//                  candidate mask (children that pass |Q| <= k and, when
-//                  enabled, the minor-min-width bound) goes to HBM.
+//                  the outside boundary of every component v touches
+//                  (children that pass |Q| <= k and, when enabled, the
+//                  minor-min-width bound). Identical children of one tile of
+//                  parents are resolved in shared memory first (tile_dedup).
 //   k_*_insert     children are flattened across the warp (warp scan +
 //                  shuffle binary search), so the atomic-heavy dedup runs one
 //                  child per lane. Bloom: 32-bit atomicOr on the reference's
 //                  bit positions, striped lock on h1 % 65536 for exactly-once
-//                  novelty, warp __match_any pre-dedup. Exact: open-addressing
-//                  table, atomicCAS claim + atomicMin on the emission rank.
+//                  novelty, warp pre-dedup. Exact: children hash-partitioned
+//                  into buckets whose distinct keys fit a shared-memory
+//                  open-addressing table (CAS claim + atomicMin on the rank).
 //   k_append       single-pass decoupled look-back scan over tiles of
 //                  parents; survivors are written in rank order (parent index
 //                  major, vertex minor) so exact mode reproduces the
@@ -39,33 +41,30 @@
 #include <string>
 
 #include "engine.hpp"
-#include "mmw.hpp"
-#include "vset.hpp"
+#include "wave_device.cuh"
 
 namespace etw {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kMaxRounds = 130;
-constexpr unsigned kFull = 0xffffffffu;
-// Bloom stripe locks. The reference uses 65,536 mutex stripes keyed by
-// h1 (bloom.cpp:18-23); any key -> stripe map keeps inserts of one key
-// serialised, and ~10^5 concurrent device threads need more stripes to keep
-// unrelated keys from contending.
-constexpr int kStripes = 1 << 20;
-constexpr unsigned kSeed1 = 0x9747B28Cu;  // bloom.hpp:24
-constexpr unsigned kSeed2 = 0x5EEDBA5Eu;  // bloom.hpp:25
-
-using u64 = unsigned long long;
-
 struct RoundStats {
     u64 expanded, offered, unique, emitted, mmw_pruned;
     u64 ticket;  // tile ticket of the round's scan pass
+    u64 winners;  // exact mode: children left after the tile pre-dedup
+    u64 np;       // exact mode: partitions of the round (power of two)
+    u64 pcap;     // exact mode: record capacity per partition
     unsigned overflowed, valid;
 };
 
-enum AbortCode : unsigned { kOk = 0, kGrowLayer = 1, kGrowTable = 2, kGrowBloom = 3, kGrowClaims = 4 };
+enum AbortCode : unsigned {
+    kOk = 0,
+    kGrowLayer = 1,    // next layer does not fit the layer buffers
+    kGrowBloom = 3,    // Bloom filter words
+    kGrowClaims = 4,   // Bloom claim table slots
+    kGrowParts = 5,    // a partition's distinct keys overflowed its shared table
+    kGrowRecs = 6,     // a partition's records overflowed its capacity
+    kGrowPartBuf = 7,  // record buffer / cursor array too small for the plan
+};
 
 struct Control {
     u64 count[2];       // layer sizes, ping-pong by round parity
@@ -76,460 +75,148 @@ struct Control {
     unsigned epoch;     // look-back tag of the current round attempt (never 0)
     unsigned exits;     // CTAs that finished the round's last pass
     unsigned pad;
+    u64 part_floor;     // exact mode: minimum partitions after a grow (per decide)
+    u64 rec_floor;      // exact mode: minimum records per partition after a grow
     RoundStats rs[kMaxRounds];
-};
-
-struct Params {
-    int n, k, rounds, free_count;
-    int hashes, bpe, any_pop, flags;  // flags: ETWG_DEBUG bits (tests only)
-    u64 max_states;
-    u64 forbidden[2];
-    u64 rows[kMaxVertices][2];
 };
 
 struct Bufs {
     u64* keys[2];
     unsigned* hist[2];
     u64* cmask;
-    u64* table;
+    u64* recs;          // exact mode: partitioned child records {key.., rank}
+    unsigned* cursors;  // exact mode: per-partition record counts (zero between rounds)
     unsigned* bloom[2];  // two filters, alternating by round parity
     unsigned* locks;
     u64* tiles;
     u64 layer_cap;   // states per layer buffer
-    u64 table_cap;   // slots
+    u64 rec_cap;     // records
+    u64 cursor_cap;  // partitions
     u64 bloom_cap;   // 32-bit words
     u64* claims;     // Bloom-mode claim table, 16-byte {key, epoch} slots
     u64 claim_cap;   // slots
 };
-
-// ----------------------------------------------------------------------
-// small device helpers
-
-template <int W>
-__device__ __forceinline__ Set<W> load_set(const u64* p, u64 i) {
-    Set<W> s;
-    if constexpr (W == 1) {
-        s.w[0] = p[i];
-    } else {
-        ulonglong2 v = reinterpret_cast<const ulonglong2*>(p)[i];
-        s.w[0] = v.x;
-        s.w[1] = v.y;
-    }
-    return s;
-}
-
-template <int W>
-__device__ __forceinline__ void store_set(u64* p, u64 i, const Set<W>& s) {
-    if constexpr (W == 1) {
-        p[i] = s.w[0];
-    } else {
-        reinterpret_cast<ulonglong2*>(p)[i] = make_ulonglong2(s.w[0], s.w[1]);
-    }
-}
-
-template <int W>
-__device__ __forceinline__ Set<W> shfl_set(const Set<W>& s, int src) {
-    Set<W> r;
-#pragma unroll
-    for (int i = 0; i < W; ++i) r.w[i] = __shfl_sync(kFull, s.w[i], src);
-    return r;
-}
-
-// position of the r-th (0-based) set bit of x; requires popc(x) > r
-__device__ __forceinline__ int nth_bit64(u64 x, int r) {
-    int pos = 0;
-#pragma unroll
-    for (int w = 32; w >= 1; w >>= 1) {
-        u64 low = x & ((u64{1} << w) - 1);
-        int c = __popcll(low);
-        if (r >= c) {
-            r -= c;
-            x >>= w;
-            pos += w;
-        }
-    }
-    return pos;
-}
-
-template <int W>
-__device__ __forceinline__ int nth_member(const Set<W>& s, int r) {
-    if constexpr (W == 1) {
-        return nth_bit64(s.w[0], r);
-    } else {
-        int c0 = __popcll(s.w[0]);
-        return r < c0 ? nth_bit64(s.w[0], r) : 64 + nth_bit64(s.w[1], r - c0);
-    }
-}
-
-// Warp-wide flattening of per-lane child masks: after scan(), iteration t
-// hands lane l the child number t*32+l in (lane, vertex) order.
-struct WarpFlat {
-    int cnt, incl, total;
-    __device__ __forceinline__ void scan(int c) {
-        const int lane = threadIdx.x & 31;
-        cnt = c;
-        incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += t;
-        }
-        total = __shfl_sync(kFull, incl, 31);
-    }
-    // lane holding child j (warp-uniform control flow required)
-    __device__ __forceinline__ int source(int j) const {
-        int src = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-            int c = __shfl_sync(kFull, incl, src + step - 1);
-            if (c <= j) src += step;
-        }
-        return src > 31 ? 31 : src;
-    }
-};
-
-__device__ __forceinline__ u64 fmix64(u64 k) {
-    k ^= k >> 33;
-    k *= 0xff51afd7ed558ccdULL;
-    k ^= k >> 33;
-    k *= 0xc4ceb9fe1a85ec53ULL;
-    k ^= k >> 33;
-    return k;
-}
-
-template <int W>
-__device__ __forceinline__ u64 slot_hash(const Set<W>& s) {
-    u64 h = fmix64(s.w[0]);
-    if constexpr (W == 2) h = fmix64(h ^ (s.w[1] + 0x9E3779B97F4A7C15ULL));
-    return h;
-}
-
-// Murmur3 x86_32 over the little-endian bytes of the key (bloom.cpp:27-64):
-// 8 bytes for n <= 64 (the reference key, bloom.cpp:66-70), 16 for n <= 128.
-__device__ __forceinline__ unsigned rotl32(unsigned x, int r) { return __funnelshift_l(x, x, r); }
-
-template <int W>
-__device__ __forceinline__ unsigned murmur_key(const Set<W>& key, unsigned seed) {
-    unsigned h = seed;
-#pragma unroll
-    for (int i = 0; i < 2 * W; ++i) {
-        unsigned k = static_cast<unsigned>(key.w[i >> 1] >> (32 * (i & 1)));
-        k *= 0xcc9e2d51u;
-        k = rotl32(k, 15);
-        k *= 0x1b873593u;
-        h ^= k;
-        h = rotl32(h, 13);
-        h = h * 5 + 0xe6546b64u;
-    }
-    h ^= 8u * W;
-    h ^= h >> 16;
-    h *= 0x85ebca6bu;
-    h ^= h >> 13;
-    h *= 0xc2b2ae35u;
-    h ^= h >> 16;
-    return h;
-}
-
-__host__ __device__ __forceinline__ u64 bloom_bits_for(u64 expected, int bpe) {
-    u64 bits = expected * static_cast<u64>(bpe);
-    u64 m = (bits + 63) / 64 * 64;  // bloom.cpp:74-75
-    return m < 64 ? 64 : m;
-}
-
-__host__ __device__ __forceinline__ u64 round_cap(const Params& p, u64 e_in) {
-    u64 upper = e_in * static_cast<u64>(p.free_count);  // dp.cpp:84-86
-    if (upper < 1) upper = 1;
-    return p.max_states < upper ? p.max_states : upper;
-}
-
-__host__ __device__ __forceinline__ u64 table_slots_for(u64 offered) {
-    u64 want = 2 * offered + 1024;
-    u64 s = 1024;
-    while (s < want) s <<= 1;
-    return s;
-}
-
-template <int W>
-__device__ __forceinline__ Set<W> param_set(const u64 (&w)[2]) {
-    Set<W> s;
-#pragma unroll
-    for (int i = 0; i < W; ++i) s.w[i] = w[i];
-    return s;
-}
-
-// ----------------------------------------------------------------------
-// K1: candidate evaluation (replaces expand_range + q_set, dp.cpp:39-69,
-// graph.hpp:61-78, and the MMW prune driven at dp.cpp:51-63)
-
-// Outside boundaries N(K) \ S of the components K of G[S]; returns count.
-template <int W>
-__device__ __forceinline__ int component_boundaries(const Set<W>* adj, const Set<W>& S,
-                                                    Set<W>* out) {
-    int nc = 0;
-    Set<W> rem = S;
-    while (rem.any()) {
-        Set<W> comp = Set<W>::bit(rem.lowest());
-        Set<W> frontier = comp;
-        Set<W> nb = Set<W>::zero();
-        while (frontier.any()) {
-            const Set<W> a = adj[frontier.pop()];
-            nb |= a;
-            Set<W> fresh = (a & S) - comp;
-            comp |= fresh;
-            frontier |= fresh;
-        }
-        rem = rem - comp;
-        Set<W> boundary = nb - S;
-        if (boundary.any()) out[nc++] = boundary;
-    }
-    return nc;
-}
-
-// Q(S,v) from the component boundaries: v's own outside neighbours plus the
-// boundary of every component adjacent to v (v lies in that boundary).
-template <int W>
-__device__ __forceinline__ Set<W> reach_from(const Set<W>* adj, const Set<W>& S, const Set<W>* bnd,
-                                             int nc, int v) {
-    Set<W> q = adj[v] - S;
-    for (int j = 0; j < nc; ++j)
-        if (bnd[j].has(v)) q |= bnd[j];
-    q.del(v);
-    return q;
-}
-
-// Minor-min-width on eliminate(G, S + v) (init_view_after, mmw.cpp:20-43,
-// then the shared contraction loop of mmw.hpp). rows[w] = Q(S,w) for every
-// w outside S. Returns early once the bound exceeds cap.
-template <int W>
-__device__ int mmw_child(const Set<W>* adj, int n, int cap, const Set<W>& S, int v,
-                         const Set<W>* rows) {
-    constexpr int N = 64 * W;
-    unsigned char parent[N];
-    unsigned char degree[N];
-    MinorState<W> m{adj, S, Set<W>::zero(), parent, degree};
-    m.elim.add(v);
-    m.alive = Set<W>::prefix(n) - m.elim;
-    for (int x = 0; x < n; ++x) {
-        parent[x] = static_cast<unsigned char>(x);
-        degree[x] = 0;
-    }
-    // eliminating v turns Q(S,v) into a clique; everyone else keeps Q(S,w)
-    for (int w : members(m.alive)) {
-        if (rows[v].has(w)) {
-            Set<W> j = rows[w] | rows[v];
-            j.del(v);
-            j.del(w);
-            degree[w] = static_cast<unsigned char>(j.count());
-        } else {
-            degree[w] = static_cast<unsigned char>(rows[w].count());
-        }
-    }
-    return minor_min_width<W>(m, cap);
-}
-
-template <int W, bool MMW>
-__device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, const Set<W>& S,
-                                             const Set<W>& forbidden, u64& pruned) {
-    constexpr int N = 64 * W;
-    const Set<W> open = Set<W>::prefix(n) - S;
-    const Set<W> eligible = open - forbidden;
-    Set<W> keep = Set<W>::zero();
-    if (eligible.none()) return keep;
-    Set<W> bnd[N];
-    const int nc = component_boundaries<W>(adj, S, bnd);
-    if constexpr (!MMW) {
-        for (int v : members(eligible))
-            if (reach_from<W>(adj, S, bnd, nc, v).count() <= k) keep.add(v);
-    } else {
-        Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
-        for (int w : members(open)) rows[w] = reach_from<W>(adj, S, bnd, nc, w);
-        for (int v : members(eligible)) {
-            if (rows[v].count() > k) continue;
-            if (mmw_child<W>(adj, n, k, S, v, rows) > k) {
-                ++pruned;
-                continue;
-            }
-            keep.add(v);
-        }
-    }
-    return keep;
-}
-
-template <int W>
-__device__ __forceinline__ void load_adjacency(const Params* P, Set<W>* adj) {
-    for (int i = threadIdx.x; i < P->n; i += blockDim.x) adj[i] = param_set<W>(P->rows[i]);
-}
 
 __device__ __forceinline__ bool halted(const Control* C) {
     return (*reinterpret_cast<const volatile unsigned*>(&C->stop) |
             *reinterpret_cast<const volatile unsigned*>(&C->abort)) != 0;
 }
 
-template <int W, bool MMW>
-__global__ void __launch_bounds__(kThreads) k_expand(const Params* __restrict__ P, Control* C,
-                                                     Bufs B) {
-    __shared__ Set<W> adj[64 * W];
-    if (halted(C)) return;
-    load_adjacency<W>(P, adj);
-    __syncthreads();
-    const unsigned r = C->round;
-    const u64 E = C->count[r & 1];
-    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-    const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
-
-    const Set<W> forbidden = param_set<W>(P->forbidden);
-    const u64* in = B.keys[r & 1];
-    u64 offered = 0, pruned = 0;
-    for (u64 idx = gtid; idx < E; idx += gstride) {
-        const Set<W> S = load_set<W>(in, idx);
-        const Set<W> keep = candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned);
-        store_set<W>(B.cmask, idx, keep);
-        offered += keep.count();
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        offered += __shfl_xor_sync(kFull, offered, o);
-        pruned += __shfl_xor_sync(kFull, pruned, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (offered) atomicAdd(&C->rs[r].offered, offered);
-        if (pruned) atomicAdd(&C->rs[r].mmw_pruned, pruned);
-    }
-}
-
 // ----------------------------------------------------------------------
-// K2a: exact dedup — open addressing, claim by CAS, keep min emission rank
-// (replaces the exact branch's sort/unique, dp.cpp:118-151)
-
-// Rank words carry a round tag in bits 48..63 that shrinks as rounds
-// advance, so any stale rank left by an earlier round of this decide loses
-// every atomicMin; keys of a round all have popcount round+1, so stale keys
-// are recognised without clearing the table between rounds.
-__device__ __forceinline__ u64 rank_tag(unsigned r) { return static_cast<u64>(kMaxRounds - r) << 48; }
-
-template <int W>
-__device__ __forceinline__ bool stale_key(const Set<W>& cur, int want_pop) {
-    return want_pop < 0 ? cur.none() : cur.count() != want_pop;
-}
-
-__device__ __forceinline__ void cas128(u64* addr, u64 exp_lo, u64 exp_hi, u64 new_lo, u64 new_hi,
-                                       u64& old_lo, u64& old_hi) {
-    asm volatile(
-        "{\n\t.reg .b128 c, s, d;\n\t"
-        "mov.b128 c, {%2, %3};\n\t"
-        "mov.b128 s, {%4, %5};\n\t"
-        "atom.global.cas.b128 d, [%6], c, s;\n\t"
-        "mov.b128 {%0, %1}, d;\n\t}"
-        : "=l"(old_lo), "=l"(old_hi)
-        : "l"(exp_lo), "l"(exp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
-        : "memory");
-}
-
-// Slot layout: W=1 {key, rank}; W=2 {key.lo, key.hi, rank, pad}.
-template <int W>
-__device__ __forceinline__ u64* table_slot(u64* table, u64 i) {
-    return table + i * (W == 1 ? 2 : 4);
-}
+// Exact dedup, partitioned (replaces the sort / unique / rank sort of the
+// exact branch, dp.cpp:118-157). A round touches each child key through a
+// global hash table only at random addresses — on a 10^9-child round that is
+// ~150 B of DRAM traffic per child. Instead the children are hash-partitioned
+// into record buckets small enough that each bucket's distinct keys fit a
+// shared-memory table:
+//   k_exact_scatter  K1 per tile of parents + tile pre-dedup; every tile
+//                    winner appends {key, rank} to bucket hash(key) >> (64-lg)
+//                    and the parent's winner mask is cleared;
+//   k_exact_part     one CTA per bucket: min emission rank per key in shared
+//                    memory, then one atomicOr per distinct key marks its
+//                    min-rank child in the parent's winner mask;
+//   k_append<W>      writes the marked children in rank order.
+// Bucket count and capacity are planned on the device from the previous
+// round's growth; an overflow aborts the round and raises the floor.
 
 template <int W>
-__device__ void table_insert(u64* table, u64 mask, int want_pop, const Set<W>& key, u64 rank) {
-    u64 i = slot_hash<W>(key) & mask;
-    for (;;) {
-        u64* slot = table_slot<W>(table, i);
-        if constexpr (W == 1) {
-            u64 cur = *reinterpret_cast<volatile u64*>(slot);
-            for (;;) {
-                if (cur == key.w[0]) break;
-                Set<1> c;
-                c.w[0] = cur;
-                if (!stale_key<1>(c, want_pop)) break;
-                u64 prev = atomicCAS(slot, cur, key.w[0]);
-                if (prev == cur) {
-                    cur = key.w[0];
-                    break;
-                }
-                cur = prev;
-            }
-            if (cur == key.w[0]) {
-                atomicMin(slot + 1, rank);
-                return;
-            }
-        } else {
-            // 128-bit keys: read through a failing CAS so the view is never torn
-            u64 lo, hi;
-            cas128(slot, ~u64{0}, ~u64{0}, ~u64{0}, ~u64{0}, lo, hi);
-            for (;;) {
-                if (lo == key.w[0] && hi == key.w[1]) break;
-                Set<2> c;
-                c.w[0] = lo;
-                c.w[1] = hi;
-                if (!stale_key<2>(c, want_pop)) break;
-                u64 plo, phi;
-                cas128(slot, lo, hi, key.w[0], key.w[1], plo, phi);
-                if (plo == lo && phi == hi) {
-                    lo = key.w[0];
-                    hi = key.w[1];
-                    break;
-                }
-                lo = plo;
-                hi = phi;
-            }
-            if (lo == key.w[0] && hi == key.w[1]) {
-                atomicMin(slot + 2, rank);
-                return;
-            }
-        }
-        i = (i + 1) & mask;
+constexpr int part_slots() { return W == 1 ? 4096 : 2048; }
+template <int W>
+constexpr int part_target() { return part_slots<W>() / 3; }  // distinct keys aimed for per bucket
+template <int W>
+constexpr int rec_words() { return W == 1 ? 2 : 4; }  // {key, rank} / {lo, hi, rank, pad}
+template <int W>
+constexpr int part_smem_bytes() { return part_slots<W>() * (8 * W + 8); }
+
+__device__ __forceinline__ u64 ceil_pow2(u64 x) {
+    u64 s = 1;
+    while (s < x) s <<= 1;
+    return s;
+}
+
+struct PartPlan {
+    u64 np, cap;
+    int lg;
+};
+
+template <int W>
+__device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C, unsigned r, u64 E) {
+    const u64 upper = E * static_cast<u64>(P->free_count > 0 ? P->free_count : 1);
+    u64 distinct = upper, winners = upper;
+    if (r > 0 && C->rs[r - 1].expanded) {
+        const double e = static_cast<double>(E) / static_cast<double>(C->rs[r - 1].expanded);
+        const u64 d = static_cast<u64>(e * static_cast<double>(C->rs[r - 1].unique) * 1.25) + 64;
+        const u64 w = static_cast<u64>(e * static_cast<double>(C->rs[r - 1].winners) * 1.25) + 64;
+        distinct = d < upper ? d : upper;
+        winners = w < upper ? w : upper;
     }
-}
-
-// After all inserts of the round: the rank stored with `key`.
-template <int W>
-__device__ __forceinline__ u64 table_rank(const u64* table, u64 mask, const Set<W>& key) {
-    u64 i = slot_hash<W>(key) & mask;
-    for (;;) {
-        const u64* slot = table + i * (W == 1 ? 2 : 4);
-        bool hit = slot[0] == key.w[0];
-        if constexpr (W == 2) hit = hit && slot[1] == key.w[1];
-        if (hit) return slot[W == 1 ? 1 : 2];
-        i = (i + 1) & mask;
-    }
+    PartPlan pl;
+    pl.np = ceil_pow2((distinct + part_target<W>() - 1) / part_target<W>());
+    if (pl.np < C->part_floor) pl.np = C->part_floor;
+    pl.lg = 0;
+    while ((u64{1} << pl.lg) < pl.np) ++pl.lg;
+    const u64 per = (winners + pl.np - 1) / pl.np;
+    pl.cap = per + per / 4 + 64;
+    if (pl.cap < C->rec_floor) pl.cap = C->rec_floor;
+    return pl;
 }
 
 template <int W>
-__device__ __forceinline__ u64 child_rank(u64 parent_idx, int v) {
-    return parent_idx * (64 * W) + static_cast<u64>(v);  // dp.cpp:66 (idx*64+v)
+__device__ __forceinline__ u64 part_of(const Set<W>& key, int lg) {
+    return lg ? slot_hash<W>(key) >> (64 - lg) : 0;
 }
 
 template <int W>
-__global__ void __launch_bounds__(kThreads) k_exact_insert(const Params* __restrict__ P,
-                                                           Control* C, Bufs B) {
+constexpr int tile_slots() { return W == 1 ? 4096 : 2048; }
+template <int W>
+constexpr int tile_set_bytes() { return static_cast<int>(sizeof(TileSet<W, tile_slots<W>()>)); }
+
+template <int W, bool MMW>
+__global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __restrict__ P, Control* C,
+                                                            Bufs B) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& ts = *reinterpret_cast<TileSet<W, tile_slots<W>()>*>(smem_raw);
+    __shared__ Set<W> adj[64 * W];
+    __shared__ unsigned win[kThreads][2 * W];
+    __shared__ unsigned s_stop;
     if (halted(C)) return;
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
-    const u64 slots = table_slots_for(C->rs[r].offered);
-    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-    if (slots > B.table_cap) {
-        if (gtid == 0) {
-            C->need = slots;
-            C->abort = kGrowTable;
+    const PartPlan pl = part_plan<W>(P, C, r, E);
+    if (pl.np > B.cursor_cap || pl.np * pl.cap > B.rec_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            C->need = pl.np * pl.cap;
+            C->abort = kGrowPartBuf;
         }
         return;
     }
-    const u64 mask = slots - 1;
-    const int want_pop = P->any_pop ? -1 : static_cast<int>(r) + 1;
-    const u64 tag = rank_tag(r);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        C->rs[r].np = pl.np;
+        C->rs[r].pcap = pl.cap;
+    }
     const int lane = threadIdx.x & 31;
-    const u64 warp = gtid >> 5;
-    const u64 nwarps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    const Set<W> forbidden = param_set<W>(P->forbidden);
     const u64* in = B.keys[r & 1];
-    for (u64 base = warp * 32; base < E; base += nwarps * 32) {
-        const u64 idx = base + lane;
+    load_adjacency<W>(P, adj);
+    const u64 ntiles = (E + kThreads - 1) / kThreads;
+    u64 offered = 0, pruned = 0, winners = 0;
+    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        tile_set_clear<W, tile_slots<W>()>(ts);
+        if (threadIdx.x == 0) s_stop = *reinterpret_cast<volatile unsigned*>(&C->abort);
+        __syncthreads();
+        if (s_stop) break;
+        const u64 idx = tile * kThreads + threadIdx.x;
         const bool valid = idx < E;
-        const Set<W> M = valid ? load_set<W>(B.cmask, idx) : Set<W>::zero();
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
+        Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
+        offered += M.count();
+        if (P->flags & 16) tile_dedup<W, tile_slots<W>()>(ts, win, S, M);  // flag 16: A/B only
+        winners += M.count();
+        if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
         WarpFlat f;
         f.scan(M.count());
+        const u64 warp_base = tile * kThreads + (threadIdx.x & ~31);
+        bool full = false;
         for (int t = 0; t < f.total; t += 32) {
             const int j = t + lane;
             const int src = f.source(j);
@@ -540,115 +227,120 @@ __global__ void __launch_bounds__(kThreads) k_exact_insert(const Params* __restr
                 const int v = nth_member<W>(Ms, j - excl);
                 Set<W> key = Ss;
                 key.add(v);
-                table_insert<W>(B.table, mask, want_pop, key, tag | child_rank<W>(base + src, v));
+                const u64 part = part_of<W>(key, pl.lg);
+                const unsigned slot = atomicAdd(B.cursors + part, 1u);
+                if (slot < pl.cap) {
+                    u64* rec = B.recs + (part * pl.cap + slot) * rec_words<W>();
+                    if constexpr (W == 1) {
+                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(warp_base + src, v));
+                    } else {
+                        *reinterpret_cast<ulonglong4*>(rec) =
+                            make_ulonglong4(key.w[0], key.w[1], child_rank<W>(warp_base + src, v), 0);
+                    }
+                } else {
+                    full = true;
+                }
             }
         }
-    }
-}
-
-// ----------------------------------------------------------------------
-// K2b: Bloom dedup on the reference's bit positions (bloom.cpp:86-97)
-
-// Stripe lock with acquire / release semantics (no full fences): the 17
-// relaxed atomicOr of a locked insert stay between the two.
-__device__ __forceinline__ void stripe_lock(unsigned* lock) {
-    unsigned old;
-    for (;;) {
-        asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "l"(lock) : "memory");
-        if (old == 0) return;
-        __nanosleep(64);
-    }
-}
-
-__device__ __forceinline__ void stripe_unlock(unsigned* lock) {
-    asm volatile("st.release.gpu.global.b32 [%0], 0;" ::"l"(lock) : "memory");
-}
-
-// Probe positions (h1 + i*h2) mod m, i = 1..hashes (bloom.cpp:90-91),
-// stepped incrementally: pos_{i+1} = pos_i + (h2 mod m) - [>= m]*m.
-__device__ __forceinline__ void probe_start(unsigned h1, unsigned h2, u64 m, u64& first, u64& step) {
-    if (m <= 0xFFFFFFFFull) {  // 32-bit division whenever m fits
-        const unsigned m32 = static_cast<unsigned>(m);
-        const unsigned s = h2 % m32;
-        const u64 f = static_cast<u64>(h1 % m32) + s;
-        step = s;
-        first = f >= m ? f - m : f;
-    } else {
-        step = static_cast<u64>(h2) % m;
-        first = (static_cast<u64>(h1) + static_cast<u64>(h2)) % m;
-    }
-}
-
-// insert_and_check (bloom.cpp:86-97) on the device. H > 0 fixes the hash
-// count at compile time so all probe loads / atomics are issued back to
-// back; H == 0 is the generic runtime-count loop.
-template <int W, int H>
-__device__ __forceinline__ bool bloom_insert_h(unsigned* bits, unsigned* locks, u64 m, int hashes,
-                                               const Set<W>& key, bool single_lock) {
-    const unsigned h1 = murmur_key<W>(key, kSeed1);
-    const unsigned h2 = murmur_key<W>(key, kSeed2);
-    u64 first, step;
-    probe_start(h1, h2, m, first, step);
-    // Fast path without the lock: when every probe bit is already set the
-    // key is a duplicate in any serialisation of the concurrent inserts
-    // (most children are: duplicates outnumber novel states ~6:1), so only
-    // inserts that can still be novel pay for the stripe lock and atomics.
-    bool all_set = true;
-    if constexpr (H > 0) {  // requires m < 2^32: positions fit 32 bits
-        unsigned pos[H];
-        unsigned word[H];
-        const unsigned m32 = static_cast<unsigned>(m), step32 = static_cast<unsigned>(step);
-        pos[0] = static_cast<unsigned>(first);
-#pragma unroll
-        for (int i = 1; i < H; ++i) {
-            const unsigned p = pos[i - 1] + step32;  // < 2m: wraps past 2^32 only if m > 2^31
-            pos[i] = (p >= m32 || p < pos[i - 1]) ? p - m32 : p;
+        if (__any_sync(kFull, full) && lane == 0) {
+            C->need = 2 * pl.cap;
+            C->abort = kGrowRecs;
         }
+        __syncthreads();
+    }
 #pragma unroll
-        for (int i = 0; i < H; ++i) word[i] = __ldcg(bits + (pos[i] >> 5));
-#pragma unroll
-        for (int i = 0; i < H; ++i) all_set &= ((word[i] >> (pos[i] & 31)) & 1u) != 0;
-        if (all_set) return false;
-        unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
-        stripe_lock(lock);
-#pragma unroll
-        for (int i = 0; i < H; ++i) word[i] = atomicOr(bits + (pos[i] >> 5), 1u << (pos[i] & 31));
-        stripe_unlock(lock);
-        bool novel = false;
-#pragma unroll
-        for (int i = 0; i < H; ++i) novel |= ((word[i] >> (pos[i] & 31)) & 1u) == 0;
-        return novel;
-    } else {
-        u64 pos = first;
-        for (int i = 1; i <= hashes; ++i) {
-            const unsigned word = __ldcg(bits + (pos >> 5));
-            all_set &= ((word >> (pos & 31)) & 1u) != 0;
-            pos += step;
-            if (pos >= m) pos -= m;
-        }
-        if (all_set) return false;
-        pos = first;
-        unsigned* lock = locks + (single_lock ? 0u : h1 % kStripes);
-        stripe_lock(lock);
-        bool novel = false;
-        for (int i = 1; i <= hashes; ++i) {
-            const unsigned bit = 1u << (pos & 31);
-            const unsigned old = atomicOr(bits + (pos >> 5), bit);
-            novel |= (old & bit) == 0;
-            pos += step;
-            if (pos >= m) pos -= m;
-        }
-        stripe_unlock(lock);
-        return novel;
+    for (int o = 16; o >= 1; o >>= 1) {
+        offered += __shfl_xor_sync(kFull, offered, o);
+        pruned += __shfl_xor_sync(kFull, pruned, o);
+        winners += __shfl_xor_sync(kFull, winners, o);
+    }
+    if (lane == 0) {
+        if (offered) atomicAdd(&C->rs[r].offered, offered);
+        if (pruned) atomicAdd(&C->rs[r].mmw_pruned, pruned);
+        if (winners) atomicAdd(&C->rs[r].winners, winners);
     }
 }
+
+constexpr int kPartThreads = 512;
 
 template <int W>
-__device__ __forceinline__ bool bloom_insert(unsigned* bits, unsigned* locks, u64 m, int hashes,
-                                             const Set<W>& key, bool single_lock = false) {
-    return hashes == 17 && m <= 0xFFFFFFFFull
-               ? bloom_insert_h<W, 17>(bits, locks, m, hashes, key, single_lock)
-               : bloom_insert_h<W, 0>(bits, locks, m, hashes, key, single_lock);
+__global__ void __launch_bounds__(kPartThreads) k_exact_part(Control* C, Bufs B) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int SLOTS = part_slots<W>();
+    u64* keys = reinterpret_cast<u64*>(smem_raw);
+    u64* ranks = keys + SLOTS * W;
+    __shared__ unsigned s_full;
+    if (halted(C)) return;
+    const unsigned r = C->round;
+    const u64 np = C->rs[r].np;
+    const u64 cap = C->rs[r].pcap;
+    for (u64 part = blockIdx.x; part < np; part += gridDim.x) {
+        for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) keys[i] = 0;
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) ranks[i] = ~u64{0};
+        if (threadIdx.x == 0) s_full = 0;
+        __syncthreads();
+        const unsigned cnt = B.cursors[part];
+        const u64* recs = B.recs + part * cap * rec_words<W>();
+        for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
+            Set<W> key;
+            u64 rank;
+            if constexpr (W == 1) {
+                const ulonglong2 rec = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + i);
+                key.w[0] = rec.x;
+                rank = rec.y;
+            } else {
+                const ulonglong2 k2 = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + 2 * i);
+                const ulonglong2 r2 = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + 2 * i + 1);
+                key.w[0] = k2.x;
+                key.w[1] = k2.y;
+                rank = r2.x;
+            }
+            unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
+            bool placed = false;
+            for (int probe = 0; probe < 128 && !placed; ++probe) {
+                if constexpr (W == 1) {
+                    const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(keys + h), 0ull, key.w[0]);
+                    placed = prev == 0 || prev == key.w[0];
+                } else {
+                    u64 lo, hi;
+                    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(keys + 2 * h));
+                    asm volatile(
+                        "{\n\t.reg .b128 c, s, d;\n\t"
+                        "mov.b128 c, {%2, %3};\n\t"
+                        "mov.b128 s, {%4, %5};\n\t"
+                        "atom.shared.cas.b128 d, [%6], c, s;\n\t"
+                        "mov.b128 {%0, %1}, d;\n\t}"
+                        : "=l"(lo), "=l"(hi)
+                        : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
+                        : "memory");
+                    placed = (lo | hi) == 0 || (lo == key.w[0] && hi == key.w[1]);
+                }
+                if (placed)
+                    atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), rank);
+                else
+                    h = (h + 1) & (SLOTS - 1);
+            }
+            if (!placed) s_full = 1;
+        }
+        __syncthreads();
+        if (s_full) {
+            if (threadIdx.x == 0) {
+                C->need = 2 * np;
+                C->abort = kGrowParts;
+            }
+            return;  // block-uniform
+        }
+        // mark each key's min-rank child in its parent's winner mask
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+            const u64 rank = ranks[i];
+            if (rank == ~u64{0}) continue;
+            const u64 parent = rank / (64 * W);
+            const int v = static_cast<int>(rank % (64 * W));
+            atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + parent * W + (v >> 6), u64{1} << (v & 63));
+        }
+        if (threadIdx.x == 0) B.cursors[part] = 0;  // clean for the next round
+        __syncthreads();
+    }
 }
 
 template <int W>
@@ -668,7 +360,7 @@ __global__ void k_bloom_batch(const u64* keys, u64 count, unsigned* bits, unsign
 // shared-memory key set (siblings of one grandparent sit next to each other
 // in the layer, so most duplicates are local), and sends the rest to the
 // global Bloom filter. The novel-children mask of every parent goes to HBM;
-// pass 2 (k_append<W,false>) turns masks into the rank-ordered next layer.
+// pass 2 (k_append<W>) turns masks into the rank-ordered next layer.
 //
 // Exactly-once novelty without the stripe-lock fences: an insert sets its
 // 17 bits with relaxed atomicOr; if any was clear it *claims* the key in an
@@ -677,94 +369,6 @@ __global__ void k_bloom_batch(const u64* keys, u64 count, unsigned* bits, unsign
 // guarantee, bloom.cpp:86-97). W=2 keys (16 bytes + tag) do not fit a
 // 16-byte CAS and use the reference's stripe locks, as does any round whose
 // claim table would exceed kClaimMax.
-
-constexpr int kWarpLocalBytes = 4096;               // per-warp key set
-constexpr int kLocalBytes = kWarpLocalBytes * (kThreads / 32);
-constexpr u64 kClaimMax = u64{1} << 27;             // slots (16 B each)
-
-// Warp-private open-addressing set (key 0 = empty; children are never the
-// empty set). True for the first inserter, and when the probe budget runs
-// out (the global filter then decides: costs dedup efficiency, never states).
-template <int W>
-__device__ __forceinline__ bool local_first(u64* slots, unsigned mask, const Set<W>& key) {
-    unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & mask;
-    for (int probe = 0; probe < 16; ++probe) {
-        if constexpr (W == 1) {
-            const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(slots + h), 0ull, key.w[0]);
-            if (prev == 0) return true;
-            if (prev == key.w[0]) return false;
-        } else {
-            u64 lo, hi;
-            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(slots + 2 * h));
-            asm volatile(
-                "{\n\t.reg .b128 c, s, d;\n\t"
-                "mov.b128 c, {%2, %3};\n\t"
-                "mov.b128 s, {%4, %5};\n\t"
-                "atom.shared.cas.b128 d, [%6], c, s;\n\t"
-                "mov.b128 {%0, %1}, d;\n\t}"
-                : "=l"(lo), "=l"(hi)
-                : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
-                : "memory");
-            if ((lo | hi) == 0) return true;
-            if (lo == key.w[0] && hi == key.w[1]) return false;
-        }
-        h = (h + 1) & mask;
-    }
-    return true;
-}
-
-// Claims a 64-bit key for this round attempt (tag = epoch) in the
-// open-addressing claim table; true iff this call is the first claim.
-__device__ __forceinline__ bool claim_key(u64* claims, u64 mask, u64 key, u64 tag) {
-    u64 i = fmix64(key ^ 0x9E3779B97F4A7C15ULL) & mask;
-    for (;;) {
-        u64* slot = claims + 2 * i;
-        // A plain 16-byte load may tear, so it only seeds the CAS: a stale
-        // tag goes straight to the claiming CAS (which fails on any tear and
-        // returns the true value); a live tag is re-read untorn first.
-        const ulonglong2 seen = __ldcg(reinterpret_cast<const ulonglong2*>(slot));
-        u64 lo = seen.x, hi = seen.y;
-        if (hi == tag) cas128(slot, ~u64{0}, ~u64{0}, ~u64{0}, ~u64{0}, lo, hi);
-        for (;;) {
-            if (hi == tag) {
-                if (lo == key) return false;
-                break;  // another key of this round: probe on
-            }
-            u64 plo, phi;
-            cas128(slot, lo, hi, key, tag, plo, phi);
-            if (plo == lo && phi == hi) return true;
-            lo = plo;
-            hi = phi;
-        }
-        i = (i + 1) & mask;
-    }
-}
-
-// Sets the key's probe bits (relaxed atomicOr); true when one was clear.
-template <int H>
-__device__ __forceinline__ bool bloom_set_bits(unsigned* bits, u64 m, u64 first, u64 step) {
-    unsigned pos[H];
-    unsigned word[H];
-    const unsigned m32 = static_cast<unsigned>(m), step32 = static_cast<unsigned>(step);
-    pos[0] = static_cast<unsigned>(first);
-#pragma unroll
-    for (int i = 1; i < H; ++i) {
-        const unsigned p = pos[i - 1] + step32;
-        pos[i] = (p >= m32 || p < pos[i - 1]) ? p - m32 : p;
-    }
-#pragma unroll
-    for (int i = 0; i < H; ++i) word[i] = __ldcg(bits + (pos[i] >> 5));
-    bool all_set = true;
-#pragma unroll
-    for (int i = 0; i < H; ++i) all_set &= ((word[i] >> (pos[i] & 31)) & 1u) != 0;
-    if (all_set) return false;  // duplicate (or false positive) in any serialisation
-#pragma unroll
-    for (int i = 0; i < H; ++i) word[i] = atomicOr(bits + (pos[i] >> 5), 1u << (pos[i] & 31));
-    bool any_clear = false;
-#pragma unroll
-    for (int i = 0; i < H; ++i) any_clear |= ((word[i] >> (pos[i] & 31)) & 1u) == 0;
-    return any_clear;
-}
 
 template <int W, bool MMW>
 __global__ void __launch_bounds__(kThreads, 3) k_bloom_dedup(const Params* __restrict__ P, Control* C,
@@ -879,39 +483,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_bloom_dedup(const Params* __res
 // (replaces the cursor append dp.cpp:96-117 and the rank sort + truncation
 // dp.cpp:150-157)
 
-// Tile status word: [epoch:24][flag:2][value:38]. The epoch changes with
-// every round attempt, so statuses left by earlier rounds read as "not yet
-// published" and the status array never needs clearing between rounds.
-constexpr u64 kFlagAgg = u64{1} << 38;
-constexpr u64 kFlagPre = u64{2} << 38;
-constexpr u64 kValMask = (u64{1} << 38) - 1;
-constexpr unsigned kEpochMask = (1u << 24) - 1;
-
-__device__ __forceinline__ u64 look_back(u64* tiles, u64 tile, u64 total, unsigned epoch) {
-    volatile u64* vt = tiles;
-    const u64 tag = static_cast<u64>(epoch & kEpochMask) << 40;
-    if (tile == 0) {
-        vt[0] = tag | kFlagPre | total;
-        return 0;
-    }
-    vt[tile] = tag | kFlagAgg | total;
-    u64 prefix = 0;
-    u64 t = tile - 1;
-    for (;;) {
-        const u64 s = vt[t];
-        if ((s >> 40) != (tag >> 40) || (s & (kFlagAgg | kFlagPre)) == 0) {
-            __nanosleep(20);
-            continue;
-        }
-        prefix += s & kValMask;
-        if (s & kFlagPre) break;
-        --t;
-    }
-    __threadfence();
-    vt[tile] = tag | kFlagPre | (prefix + total);
-    return prefix;
-}
-
 // Writes the tile's survivors (mask M over parents S with histories H) in
 // rank order: the warp's survivors occupy one contiguous run starting at
 // warp_start, so consecutive lanes store consecutive states.
@@ -969,12 +540,11 @@ __device__ __forceinline__ void finish_round(const Params* P, Control* C, const 
     if (emitted == 0 || static_cast<int>(r) + 1 >= P->rounds) C->stop = 1;
 }
 
-template <int W, bool PROBE>
+template <int W>
 __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ P, Control* C,
                                                      Bufs B) {
     using BlockScan = cub::BlockScan<unsigned, kThreads>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
-    __shared__ unsigned win_words[kThreads][2 * W];
     __shared__ u64 s_prefix;
     __shared__ u64 s_tile;
     if (halted(C)) return;
@@ -984,10 +554,6 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
     const u64 ntiles = (E + kThreads - 1) / kThreads;
     const u64 cap = round_cap(*P, E);
     const u64 limit = cap < B.layer_cap ? cap : B.layer_cap;
-    const u64 slots = PROBE ? table_slots_for(C->rs[r].offered) : 0;
-    const u64 tag = rank_tag(r);
-    const int lane = threadIdx.x & 31;
-    const int wslot = threadIdx.x & ~31;
     const u64* in = B.keys[r & 1];
     const unsigned* hin = B.hist[r & 1];
     u64* out = B.keys[(r + 1) & 1];
@@ -1002,36 +568,7 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
         const unsigned H = valid ? hin[idx] : 0u;
-        Set<W> M = valid ? load_set<W>(B.cmask, idx) : Set<W>::zero();
-        if constexpr (PROBE) {
-            // winners: children whose stored min rank is their own
-#pragma unroll
-            for (int i = 0; i < 2 * W; ++i) win_words[threadIdx.x][i] = 0;
-            __syncwarp();
-            WarpFlat f;
-            f.scan(M.count());
-            const u64 warp_base = tile * kThreads + wslot;
-            for (int t = 0; t < f.total; t += 32) {
-                const int j = t + lane;
-                const int src = f.source(j);
-                const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
-                const Set<W> Ms = shfl_set<W>(M, src);
-                const Set<W> Ss = shfl_set<W>(S, src);
-                if (j < f.total) {
-                    const int v = nth_member<W>(Ms, j - excl);
-                    Set<W> key = Ss;
-                    key.add(v);
-                    const u64 mine = tag | child_rank<W>(warp_base + src, v);
-                    if (table_rank<W>(B.table, slots - 1, key) == mine)
-                        atomicOr(&win_words[wslot + src][v >> 5], 1u << (v & 31));
-                }
-            }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < W; ++i)
-                M.w[i] = win_words[threadIdx.x][2 * i] |
-                         (static_cast<u64>(win_words[threadIdx.x][2 * i + 1]) << 32);
-        }
+        const Set<W> M = valid ? load_set<W>(B.cmask, idx) : Set<W>::zero();
         const unsigned cnt = static_cast<unsigned>(M.count());
         unsigned excl_block, total_block;
         BlockScan(scan_tmp).ExclusiveSum(cnt, excl_block, total_block);
@@ -1047,22 +584,6 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
         __syncthreads();
     }
     finish_round(P, C, B, r, E, cap);
-}
-
-// ----------------------------------------------------------------------
-// table reset for a new decide (keys 0, ranks all-ones)
-
-template <int W>
-__global__ void k_table_reset(u64* table, u64 slots) {
-    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-    const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
-    for (u64 i = gtid; i < slots; i += gstride) {
-        if constexpr (W == 1) {
-            reinterpret_cast<ulonglong2*>(table)[i] = make_ulonglong2(0, ~u64{0});
-        } else {
-            reinterpret_cast<ulonglong4*>(table)[i] = make_ulonglong4(0, 0, ~u64{0}, 0);
-        }
-    }
 }
 
 // ----------------------------------------------------------------------
@@ -1128,7 +649,6 @@ public:
         unsigned root_hist = 0xFFFFFFFFu;
         copy(b_.keys[0], zero2, 16, cudaMemcpyHostToDevice, "root");
         copy(b_.hist[0], &root_hist, 4, cudaMemcpyHostToDevice, "root");
-        if (cfg.dedup == DedupMode::exact_set) reset_table(W);
 
         run_rounds(W, cfg, rounds, k, observer);
 
@@ -1185,7 +705,6 @@ public:
         }
         copy(b_.keys[0], keys.data(), keys.size() * 8, cudaMemcpyHostToDevice, "expand input");
         copy(b_.hist[0], hist.data(), hist.size() * 4, cudaMemcpyHostToDevice, "expand input");
-        if (cfg.dedup == DedupMode::exact_set) reset_table(W);
         run_rounds(W, cfg, 1, k, nullptr);
         const RoundStats& s = h_ctl_->rs[0];
         stats.emitted = s.emitted;
@@ -1244,11 +763,12 @@ private:
     Control* d_ctl_ = nullptr;
     Control* h_ctl_ = nullptr;
     Bufs b_{};
-    u64 table_dirty_bytes_ = 0;  // table bytes possibly holding keys of an earlier decide
     u64 bloom_dirty_[2] = {0, 0};  // words of each Bloom filter that may hold bits
     unsigned epoch_ = 1;          // look-back epoch carried across decides
     bool bloom_round_ = false;    // current decide runs the fused Bloom round
     int grid_fused_ = 0;
+    int grid_exact_[2] = {0, 0};
+    int grid_part_[2] = {0, 0};
 
     // Epochs tag look-back statuses (24 bits); on wrap-around the status
     // array is cleared so a status from 2^24 attempts ago cannot match.
@@ -1260,7 +780,6 @@ private:
         }
         return epoch_;
     }
-    int table_layout_ = 0;       // slot layout (W) the clean part of the table is in
     int grid_ = 0;
     cudaEvent_t ev_[2] = {nullptr, nullptr};
     cudaEvent_t tev_[2] = {nullptr, nullptr};
@@ -1302,6 +821,27 @@ private:
                                                             kLocalBytes),
               "occupancy");
         grid_fused_ = prop.multiProcessorCount * std::max(1, per_sm);
+        auto allow_exact = [&](auto kernel, int bytes, int& grid) {
+            check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                  "smem attribute");
+            int blocks = 0;
+            check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, bytes), "occupancy");
+            grid = prop.multiProcessorCount * std::max(1, blocks);
+        };
+        allow_exact(k_exact_scatter<1, false>, tile_set_bytes<1>(), grid_exact_[0]);
+        allow_exact(k_exact_scatter<1, true>, tile_set_bytes<1>(), grid_exact_[0]);
+        allow_exact(k_exact_scatter<2, false>, tile_set_bytes<2>(), grid_exact_[1]);
+        allow_exact(k_exact_scatter<2, true>, tile_set_bytes<2>(), grid_exact_[1]);
+        auto allow_part = [&](auto kernel, int bytes, int& grid) {
+            check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                  "smem attribute");
+            int blocks = 0;
+            check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kPartThreads, bytes),
+                  "occupancy");
+            grid = prop.multiProcessorCount * std::max(1, blocks);
+        };
+        allow_part(k_exact_part<1>, part_smem_bytes<1>(), grid_part_[0]);
+        allow_part(k_exact_part<2>, part_smem_bytes<2>(), grid_part_[1]);
         check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
         check(cudaMalloc(&d_params_, sizeof(Params)), "malloc params");
         check(cudaMallocHost(&h_params_, sizeof(Params)), "host params");
@@ -1387,14 +927,26 @@ private:
         b_.layer_cap = cap;
     }
 
-    void ensure_table(u64 slots) {
-        if (slots <= b_.table_cap && b_.table) return;
-        u64 cap = std::max<u64>(slots, u64{1} << 20);
-        if (b_.table) cudaFree(b_.table);
-        check(cudaMalloc(&b_.table, cap * 32), "table");
-        b_.table_cap = cap;
-        table_dirty_bytes_ = cap * 32;  // fresh memory: reset everything before use
-        table_layout_ = 0;
+    // Exact-mode record buckets; cursors start (and are left by every
+    // completed round) at zero.
+    void ensure_parts(u64 recs, u64 parts) {
+        if (recs > b_.rec_cap || !b_.recs) {
+            const u64 cap = std::max<u64>(recs, u64{1} << 20);
+            if (b_.recs) cudaFree(b_.recs);
+            check(cudaMalloc(&b_.recs, cap * 32), "records");
+            b_.rec_cap = cap;
+        }
+        if (parts > b_.cursor_cap || !b_.cursors) {
+            const u64 cap = std::max<u64>(parts, u64{1} << 16);
+            if (b_.cursors) cudaFree(b_.cursors);
+            check(cudaMalloc(&b_.cursors, cap * 4), "cursors");
+            check(cudaMemsetAsync(b_.cursors, 0, cap * 4, stream_), "cursors zero");
+            b_.cursor_cap = cap;
+        }
+    }
+
+    void clean_cursors() {
+        check(cudaMemsetAsync(b_.cursors, 0, b_.cursor_cap * 4, stream_), "cursors clean");
     }
 
     void ensure_bloom(u64 words) {
@@ -1445,28 +997,6 @@ private:
         return std::min<u64>(h_params_->max_states, upper);
     }
 
-    // The "empty" pattern differs between the 16-byte (W=1) and 32-byte
-    // (W=2) slot layouts, so switching layouts re-initialises the whole table.
-    void reset_table(int W) {
-        ensure_table(u64{1} << 20);
-        if (W != table_layout_) {
-            table_dirty_bytes_ = b_.table_cap * 32;
-            table_layout_ = W;
-        }
-        if (table_dirty_bytes_ == 0) return;
-        const u64 slot_bytes = W == 1 ? 16 : 32;
-        u64 slots = std::min((table_dirty_bytes_ + slot_bytes - 1) / slot_bytes,
-                             b_.table_cap * 32 / slot_bytes);
-        int blocks = static_cast<int>(std::min<u64>((slots + 255) / 256, 4096));
-        if (W == 1)
-            k_table_reset<1><<<blocks, 256, 0, stream_>>>(b_.table, slots);
-        else
-            k_table_reset<2><<<blocks, 256, 0, stream_>>>(b_.table, slots);
-        check(cudaGetLastError(), "table reset");
-        prof.t.kernel_launches++;
-        table_dirty_bytes_ = 0;
-    }
-
     template <int W>
     void launch_round(const DpConfig& cfg) {
         const bool exact = cfg.dedup == DedupMode::exact_set;
@@ -1492,19 +1022,19 @@ private:
             else
                 timed_launch([&] { k_bloom_dedup<W, false><<<grid_fused_, kThreads, kLocalBytes, stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.insert_ms, prof.t.insert_launches);
-            timed_launch([&] { k_append<W, false><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_append<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.append_ms, prof.t.append_launches);
             return;
         }
         if (cfg.use_mmw)
-            timed_launch([&] { k_expand<W, true><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_exact_scatter<W, true><<<grid_exact_[W - 1], kThreads, tile_set_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
         else
-            timed_launch([&] { k_expand<W, false><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_exact_scatter<W, false><<<grid_exact_[W - 1], kThreads, tile_set_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
-        timed_launch([&] { k_exact_insert<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
+        timed_launch([&] { k_exact_part<W><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_ctl_, b_); },
                      prof.t.insert_ms, prof.t.insert_launches);
-        timed_launch([&] { k_append<W, true><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
+        timed_launch([&] { k_append<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
                      prof.t.append_ms, prof.t.append_launches);
     }
 
@@ -1522,7 +1052,7 @@ private:
     }
 
     void run_rounds(int W, const DpConfig& cfg, int rounds, int k, const LayerObserver* observer) {
-        ensure_table(u64{1} << 20);
+        ensure_parts(u64{1} << 20, u64{1} << 22);
         ensure_bloom(u64{1} << 22);
         ensure_claims(u64{1} << 20);
         bloom_round_ = cfg.dedup == DedupMode::bloom;
@@ -1563,13 +1093,6 @@ private:
                     bloom_dirty_[last & 1],
                     bloom_bits_for(host_round_cap(h_ctl_->rs[last].expanded), h_params_->bpe) / 32);
         }
-        if (cfg.dedup == DedupMode::exact_set) {
-            const u64 slot_bytes = W == 1 ? 16 : 32;
-            for (int r = 0; r < rounds; ++r)
-                if (h_ctl_->rs[r].offered)
-                    table_dirty_bytes_ = std::max(
-                        table_dirty_bytes_, table_slots_for(h_ctl_->rs[r].offered) * slot_bytes);
-        }
         if (!prof.on) {
             check(cudaEventRecord(ev_[1], stream_), "event");
             check(cudaEventSynchronize(ev_[1]), "event sync");
@@ -1595,9 +1118,17 @@ private:
                     clean_blooms();
                 }
                 break;
-            case kGrowTable:
-                ensure_table(c.need);  // fresh memory, fully reset below
-                reset_table(W);
+            case kGrowParts:
+                c.part_floor = std::max<u64>(c.part_floor, c.need);
+                clean_cursors();
+                break;
+            case kGrowRecs:
+                c.rec_floor = std::max<u64>(c.rec_floor, c.need);
+                clean_cursors();
+                break;
+            case kGrowPartBuf:
+                ensure_parts(c.need + c.need / 4, 0);
+                clean_cursors();
                 break;
             case kGrowBloom:
                 ensure_bloom(c.need + c.need / 4);
