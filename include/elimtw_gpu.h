@@ -73,7 +73,8 @@ ELIMTW_API uint64_t etwg_bloom_insert(uint64_t expected, int bits_per_element, i
  * out[0..] = decide_ms, expand_ms, insert_ms, append_ms, clear_ms, fused_ms,
  * expand_launches, insert_launches, append_launches, clear_launches,
  * fused_launches, kernel_launches, layer_bytes, dedup_bytes, expanded,
- * h2d_bytes, d2h_bytes. Returns the number of values written. */
+ * h2d_bytes, d2h_bytes, exchange_bytes, reruns. Returns the number of values
+ * written. */
 ELIMTW_API int etwg_times(double* out, int len);
 /* CUDA events on the engine stream around a region; end synchronizes and
  * returns the device milliseconds in between. */
@@ -81,6 +82,28 @@ ELIMTW_API void etwg_timer_begin(void);
 ELIMTW_API double etwg_timer_end(void);
 ELIMTW_API void etwg_set_profiling(int on);
 ELIMTW_API void etwg_reset_times(void);
+
+/* Owner-sharded decides. While sharding is active every decide
+ * of this process — etw_solve's included — runs as one shard of G: each
+ * layer state lives on shard owner(S), children are routed to their owners
+ * every round and a per-round count allgather decides termination.
+ *
+ *   etwg_set_virtual_shards(G)   G (1..8) virtual shards on this process's
+ *                                device, exchanging through device copies:
+ *                                the single-GPU double of the NCCL path; 1 = off.
+ *   etwg_nccl_unique_id(id)      128-byte ncclUniqueId (rank 0 makes it, the
+ *                                caller distributes it, e.g. torch.distributed)
+ *   etwg_shard_init(id, rank, world, device)
+ *                                one shard per process over NCCL; every rank
+ *                                must then make the same sequence of solves
+ *   etwg_shard_release()         back to the single-device engine
+ *   etwg_shard_info              world size, rank, 1 when virtual            */
+ELIMTW_API etw_status etwg_set_virtual_shards(int shards, char* err, size_t err_len);
+ELIMTW_API etw_status etwg_nccl_unique_id(uint8_t* id128, char* err, size_t err_len);
+ELIMTW_API etw_status etwg_shard_init(const uint8_t* id128, int rank, int world, int device, char* err,
+                                      size_t err_len);
+ELIMTW_API void etwg_shard_release(void);
+ELIMTW_API void etwg_shard_info(int* world, int* rank, int* is_virtual);
 
 /* host preprocessing (no GPU needed); rows as above */
 ELIMTW_API void etwg_graph_rows(const etw_graph* g, uint64_t* rows);

@@ -421,11 +421,60 @@ int etwg_times(double* out, int len) {
                         t.dedup_bytes,
                         static_cast<double>(t.expanded),
                         static_cast<double>(t.h2d_bytes),
-                        static_cast<double>(t.d2h_bytes)};
+                        static_cast<double>(t.d2h_bytes),
+                        t.exchange_bytes,
+                        static_cast<double>(t.reruns)};
     int n = static_cast<int>(sizeof v / sizeof v[0]);
     if (len < n) n = len;
     for (int i = 0; i < n; ++i) out[i] = v[i];
     return n;
+}
+
+etw_status etwg_set_virtual_shards(int shards, char* err, size_t err_len) {
+    try {
+        shard_set_virtual(shards);
+        return ETW_OK;
+    } catch (...) {
+        return status_of_current_exception(err, err_len);
+    }
+}
+
+etw_status etwg_nccl_unique_id(uint8_t* id128, char* err, size_t err_len) {
+    if (!id128) return ETW_ERROR_INVALID_ARGUMENT;
+    try {
+        shard_unique_id(id128);
+        return ETW_OK;
+    } catch (...) {
+        return status_of_current_exception(err, err_len);
+    }
+}
+
+etw_status etwg_shard_init(const uint8_t* id128, int rank, int world, int device, char* err,
+                           size_t err_len) {
+    if (!id128) return ETW_ERROR_INVALID_ARGUMENT;
+    try {
+        shard_init_nccl(id128, rank, world, device);
+        return ETW_OK;
+    } catch (...) {
+        return status_of_current_exception(err, err_len);
+    }
+}
+
+void etwg_shard_release(void) {
+    try {
+        shard_release();
+    } catch (...) {
+    }
+}
+
+void etwg_shard_info(int* world, int* rank, int* is_virtual) {
+    try {
+        shard_info(world, rank, is_virtual);
+    } catch (...) {
+        if (world) *world = 1;
+        if (rank) *rank = 0;
+        if (is_virtual) *is_virtual = 0;
+    }
 }
 
 void etwg_set_profiling(int on) { engine_set_profiling(on != 0); }

@@ -103,6 +103,8 @@ struct KernelTimes {
     double decide_ms = 0;          // device time of decide calls (events)
     uint64_t expanded = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of the engine
+    double exchange_bytes = 0;  // sharded: child records sent to other shards
+    uint64_t reruns = 0;        // sharded: rounds re-run after a buffer grew
 };
 // Brackets a region on the engine's stream with CUDA events; end returns the
 // device milliseconds between the two events (synchronizing).
@@ -111,5 +113,22 @@ double engine_timer_end();
 void engine_set_profiling(bool on);
 KernelTimes engine_times();
 void engine_reset_times();
+
+// Owner-sharded decide over G shards (shard.cu). Active after
+// shard_set_virtual(G > 1) — G virtual shards on this process's device, the
+// single-GPU test double of the exchange — or shard_init_nccl (one shard per
+// process/GPU, NCCL over NVLink). device_decide routes to it while active.
+bool shard_active();
+DecideResult shard_decide(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg, int rounds,
+                          const LayerObserver* observer);
+void shard_set_virtual(int G);
+void shard_unique_id(unsigned char* out128);
+void shard_init_nccl(const unsigned char* id128, int rank, int world, int device);
+void shard_release();
+void shard_info(int* world, int* rank, int* virt);
+void shard_timer_begin();
+double shard_timer_end();
+void shard_accumulate(KernelTimes& t);
+void shard_reset_times();
 
 }  // namespace etw

@@ -1,0 +1,1111 @@
+// Owner-sharded wavefront across G devices: the multi-GPU
+// replacement for the reference's decide / expand_layer (proj/src/dp.cpp:
+// 73-194), one shard per B200.
+//
+// Every state S of a layer lives on its owner shard owner(S) =
+// mulhi(mix(S), G) (a hash independent of the partition hash and of the Bloom
+// probes). A round on every shard:
+//
+//   k_route   K1 (candidates, graph.hpp:61-78 / dp.cpp:39-69) over the local
+//             parents; each child {S+v, rank, history} is appended to the
+//             outbox bucket (owner, partition) — partition = top bits of an
+//             independent hash, sized so one bucket's distinct keys fit a
+//             shared-memory table.
+//   exchange  outbox block d -> inbox slot `me` of shard d, with its bucket
+//             counts: NCCL grouped send/recv over NVLink (one process per
+//             GPU), or device copies between virtual shards of one device.
+//   k_owner   per partition, in partition order: exact dedup of the records
+//             every source sent (min emission rank per key, the history of
+//             the min-rank emission — dp.cpp:140-151 semantics), optional
+//             Bloom filter on the owner's slice (bloom.cpp:86-97), rank sort,
+//             ordered append to the local next layer (decoupled look-back).
+//   allgather per-shard counters (ncclAllGather / copies) — the per-level
+//             count reduction that decides termination (dp.cpp:176-188).
+//   k_finish  global stats, the capacity wall applied shard-major
+//             (emitted = min(unique, cap), dp.cpp:84-86, 152-155), next round.
+//
+// Exact-mode per-level sets and counters (expanded, emitted, duplicates,
+// mmw_pruned) equal the single-device engine's; layer order is
+// (partition, source shard, parent index, vertex), deterministic for a
+// given G. The host plans each round's bucket geometry from the previous
+// round's growth and re-runs a round whose buckets overflowed.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "engine.hpp"
+#include "wave_device.cuh"
+
+namespace etw {
+
+namespace {
+
+constexpr int kMaxShards = 8;
+constexpr int kOwnerThreads = 512;
+constexpr int kRouteThreads = 256;
+
+template <int W>
+constexpr int owner_slots() { return 2048; }
+template <int W>
+constexpr int owner_target() { return 640; }  // distinct keys aimed for per partition
+template <int W>
+constexpr int srec_words() { return W + 2; }  // {key words, rank, history}
+template <int W>
+constexpr int owner_smem_bytes() {
+    return owner_slots<W>() * (8 * W + 8 + 4 + 8);  // keys, ranks, histories, sort keys
+}
+
+enum ShardAbort : unsigned { kAbortLayer = 1, kAbortRecs = 2, kAbortParts = 4 };
+
+struct ShardStat {
+    u64 expanded, offered, pruned, routed, unique;
+    u64 need_layer, need_recs, need_parts;
+    unsigned abort, pad;
+};
+
+struct ShardRound {
+    u64 expanded, offered, unique, emitted, pruned, routed;
+    unsigned overflowed, valid;
+};
+
+struct ShardCtl {
+    u64 count[2];  // local layer sizes, ping-pong by round parity
+    unsigned round, stop, epoch, pad;
+    u64 ticket;  // owner-pass partition ticket
+    ShardStat mine;
+    ShardStat all[kMaxShards];
+    ShardRound rs[kMaxRounds];
+};
+
+// Round geometry, identical on every shard (host-planned).
+struct Plan {
+    u64 np;       // partitions per owner (power of two)
+    u64 cap;      // records per (owner, partition) bucket of one source
+    u64 bloom_m;  // bits of the owner's Bloom slice (0: exact mode)
+    u64 layer_est;  // host sizing hint: next-layer states per owner
+    int lg, G, me, rounds;
+};
+
+struct ShardBufs {
+    u64* keys[2];
+    unsigned* hist[2];
+    u64 layer_cap;
+    u64* out;            // outbox: [owner][partition][cap] records
+    unsigned* out_cnt;   // [owner][partition]
+    u64* in;             // inbox: [source][partition][cap] records
+    unsigned* in_cnt;    // [source][partition]
+    u64 box_cap;         // records per box
+    u64 cnt_cap;         // counters per box
+    u64* tiles;          // look-back status per partition
+    u64 tile_cap;
+    unsigned* bloom;     // the owner's Bloom slice (32-bit words)
+    u64 bloom_cap;       // words
+};
+
+template <int W>
+__device__ __forceinline__ unsigned owner_of(const Set<W>& key, int G) {
+    u64 h = fmix64(key.w[0] ^ 0xD6E8FEB86659FD93ULL);
+    if constexpr (W == 2) h = fmix64(h ^ key.w[1]);
+    return static_cast<unsigned>(__umul64hi(h, static_cast<u64>(G)));
+}
+
+// partition of a key inside its owner: top bits of the slot hash (the
+// shared-memory table of k_owner indexes with the low bits)
+template <int W>
+__device__ __forceinline__ u64 part_hash_bits(const Set<W>& key, int lg) {
+    return lg ? slot_hash<W>(key) >> (64 - lg) : 0;
+}
+
+// ----------------------------------------------------------------------
+// k_route: candidates of the local parents, children to owner buckets
+
+template <int W, bool MMW>
+__global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restrict__ P, ShardCtl* C,
+                                                         ShardBufs B, Plan pl) {
+    __shared__ Set<W> adj[64 * W];
+    if (C->stop) return;
+    const unsigned r = C->round;
+    const u64 E = C->count[r & 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) C->mine.expanded = E;
+    load_adjacency<W>(P, adj);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const Set<W> forbidden = param_set<W>(P->forbidden);
+    const u64* in = B.keys[r & 1];
+    const unsigned* hin = B.hist[r & 1];
+    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+    const u64 nwarps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    const u64 src_tag = static_cast<u64>(pl.me) << 40;
+    u64 offered = 0, pruned = 0;
+    bool full = false;
+    for (u64 base = (gtid >> 5) * 32; base < E; base += nwarps * 32) {
+        const u64 idx = base + lane;
+        const bool valid = idx < E;
+        const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
+        const unsigned H = valid ? hin[idx] : 0u;
+        const Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
+        offered += M.count();
+        WarpFlat f;
+        f.scan(M.count());
+        for (int t = 0; t < f.total; t += 32) {
+            const int j = t + lane;
+            const int src = f.source(j);
+            const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
+            const Set<W> Ms = shfl_set<W>(M, src);
+            const Set<W> Ss = shfl_set<W>(S, src);
+            const unsigned Hs = __shfl_sync(kFull, H, src);
+            if (j < f.total) {
+                const int v = nth_member<W>(Ms, j - excl);
+                Set<W> key = Ss;
+                key.add(v);
+                const u64 bucket = static_cast<u64>(owner_of<W>(key, pl.G)) * pl.np + part_hash_bits<W>(key, pl.lg);
+                const unsigned slot = atomicAdd(B.out_cnt + bucket, 1u);
+                if (slot < pl.cap) {
+                    u64* rec = B.out + (bucket * pl.cap + slot) * srec_words<W>();
+#pragma unroll
+                    for (int w = 0; w < W; ++w) rec[w] = key.w[w];
+                    rec[W] = src_tag | child_rank<W>(base + src, v);
+                    rec[W + 1] = (static_cast<u64>(Hs) << 8) | static_cast<u64>(v & 0xFF);  // push_history
+                } else {
+                    full = true;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        offered += __shfl_xor_sync(kFull, offered, o);
+        pruned += __shfl_xor_sync(kFull, pruned, o);
+    }
+    full = __any_sync(kFull, full);
+    if (lane == 0) {
+        if (offered) {
+            atomicAdd(&C->mine.offered, offered);
+            atomicAdd(&C->mine.routed, offered);
+        }
+        if (pruned) atomicAdd(&C->mine.pruned, pruned);
+        if (full) {
+            atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortRecs));
+            atomicMax(&C->mine.need_recs, 2 * pl.cap);
+        }
+    }
+}
+
+// ----------------------------------------------------------------------
+// k_owner: per partition exact dedup (+ Bloom), rank sort, ordered append
+
+template <int W>
+__device__ __forceinline__ void load_srec(const u64* rec, Set<W>& key, u64& rank, unsigned& hist) {
+    if constexpr (W == 1) {
+        key.w[0] = __ldcs(rec);
+    } else {
+        const ulonglong2 k2 = __ldcs(reinterpret_cast<const ulonglong2*>(rec));
+        key.w[0] = k2.x;
+        key.w[1] = k2.y;
+    }
+    rank = __ldcs(rec + W);
+    hist = static_cast<unsigned>(__ldcs(rec + W + 1));
+}
+
+template <int W, bool BLOOM>
+__global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restrict__ P, ShardCtl* C,
+                                                         ShardBufs B, Plan pl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int SLOTS = owner_slots<W>();
+    u64* keys = reinterpret_cast<u64*>(smem_raw);
+    u64* ranks = keys + SLOTS * W;
+    u64* sortk = ranks + SLOTS;
+    unsigned* hists = reinterpret_cast<unsigned*>(sortk + SLOTS);
+    __shared__ unsigned s_full, s_cnt;
+    __shared__ u64 s_part, s_prefix;
+    if (C->stop) return;
+    const unsigned r = C->round;
+    const unsigned epoch = C->epoch;
+    u64* out = B.keys[(r + 1) & 1];
+    unsigned* hout = B.hist[(r + 1) & 1];
+    for (;;) {
+        if (threadIdx.x == 0) s_part = atomicAdd(&C->ticket, 1ull);
+        __syncthreads();
+        const u64 part = s_part;
+        if (part >= pl.np) break;
+        for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) keys[i] = 0;
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) ranks[i] = ~u64{0};
+        if (threadIdx.x == 0) {
+            s_full = 0;
+            s_cnt = 0;
+        }
+        __syncthreads();
+        // pass 1: every source's records of this partition -> min rank per key
+        for (int s = 0; s < pl.G; ++s) {
+            const u64 bucket = static_cast<u64>(s) * pl.np + part;
+            const unsigned cnt = min(B.in_cnt[bucket], static_cast<unsigned>(pl.cap));
+            const u64* recs = B.in + bucket * pl.cap * srec_words<W>();
+            for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
+                Set<W> key;
+                u64 rank;
+                unsigned hist;
+                load_srec<W>(recs + static_cast<u64>(i) * srec_words<W>(), key, rank, hist);
+                unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
+                bool placed = false;
+                for (int probe = 0; probe < SLOTS && !placed; ++probe) {
+                    placed = smem_claim<W>(keys, h, key);
+                    if (!placed) h = (h + 1) & (SLOTS - 1);
+                }
+                if (placed)
+                    atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), rank);
+                else
+                    s_full = 1;
+            }
+        }
+        __syncthreads();
+        const bool full = s_full != 0;
+        if (!full) {
+            // pass 2: the min-rank record of each key leaves its history
+            for (int s = 0; s < pl.G; ++s) {
+                const u64 bucket = static_cast<u64>(s) * pl.np + part;
+                const unsigned cnt = min(B.in_cnt[bucket], static_cast<unsigned>(pl.cap));
+                const u64* recs = B.in + bucket * pl.cap * srec_words<W>();
+                for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
+                    Set<W> key;
+                    u64 rank;
+                    unsigned hist;
+                    load_srec<W>(recs + static_cast<u64>(i) * srec_words<W>(), key, rank, hist);
+                    const int slot = smem_find<W>(keys, static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1),
+                                                  SLOTS - 1, key, SLOTS);
+                    if (slot >= 0 && ranks[slot] == rank) hists[slot] = hist;
+                }
+            }
+            __syncthreads();
+            // compact the distinct keys (Bloom mode: only those the filter calls novel)
+            for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+                if (ranks[i] == ~u64{0}) continue;
+                bool keep = true;
+                if constexpr (BLOOM) {
+                    Set<W> key;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) key.w[w] = keys[W * i + w];
+                    const unsigned h1 = murmur_key<W>(key, kSeed1);
+                    const unsigned h2 = murmur_key<W>(key, kSeed2);
+                    u64 pos, step;
+                    probe_start(h1, h2, pl.bloom_m, pos, step);
+                    // distinct keys of one round meet the filter exactly once, so the
+                    // reference's "any probed bit was clear" is the novelty test
+                    keep = false;
+                    for (int t = 1; t <= P->hashes; ++t) {
+                        const unsigned bit = 1u << (pos & 31);
+                        keep |= (atomicOr(B.bloom + (pos >> 5), bit) & bit) == 0;
+                        pos += step;
+                        if (pos >= pl.bloom_m) pos -= pl.bloom_m;
+                    }
+                }
+                if (keep) sortk[atomicAdd(&s_cnt, 1u)] = (ranks[i] << 12) | static_cast<u64>(i);
+            }
+        }
+        __syncthreads();
+        const unsigned cnt = full ? 0u : s_cnt;
+        // bitonic sort of the partition's survivors by emission rank
+        unsigned m = 1;
+        while (m < cnt) m <<= 1;
+        for (unsigned i = cnt + threadIdx.x; i < m; i += blockDim.x) sortk[i] = ~u64{0};
+        __syncthreads();
+        for (unsigned size = 2; size <= m; size <<= 1) {
+            for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+                for (unsigned i = threadIdx.x; i < m; i += blockDim.x) {
+                    const unsigned j = i ^ stride;
+                    if (j > i) {
+                        const u64 a = sortk[i], b = sortk[j];
+                        const bool up = (i & size) == 0;
+                        if ((a > b) == up) {
+                            sortk[i] = b;
+                            sortk[j] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // every claimed partition publishes its count, even an aborted one
+        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, part, cnt, epoch);
+        __syncthreads();
+        const u64 prefix = s_prefix;
+        for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const u64 pos = prefix + i;
+            if (pos >= B.layer_cap) break;
+            const int slot = static_cast<int>(sortk[i] & 0xFFF);
+            Set<W> key;
+#pragma unroll
+            for (int w = 0; w < W; ++w) key.w[w] = keys[W * slot + w];
+            store_set<W>(out, pos, key);
+            hout[pos] = hists[slot];
+        }
+        if (threadIdx.x == 0) {
+            if (full) {
+                atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortParts));
+                atomicMax(&C->mine.need_parts, 2 * pl.np);
+            }
+            if (prefix + cnt > B.layer_cap) {
+                atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortLayer));
+                atomicMax(&C->mine.need_layer, prefix + cnt);
+            }
+            if (part == pl.np - 1) C->mine.unique = prefix + cnt;
+        }
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------------
+// k_finish: global counters (all[] holds every shard's ShardStat)
+
+__global__ void k_shard_finish(const Params* __restrict__ P, ShardCtl* C, Plan pl) {
+    if (threadIdx.x != 0 || C->stop) return;
+    unsigned abort = 0;
+    u64 E = 0, offered = 0, pruned = 0, unique = 0, routed = 0, before = 0;
+    for (int s = 0; s < pl.G; ++s) {
+        const ShardStat& st = C->all[s];
+        abort |= st.abort;
+        E += st.expanded;
+        offered += st.offered;
+        pruned += st.pruned;
+        unique += st.unique;
+        routed += st.routed;
+        if (s < pl.me) before += st.unique;
+    }
+    if (abort) return;  // the host grows what the round asked for and re-runs it
+    const unsigned r = C->round;
+    const u64 cap = round_cap(*P, E);
+    const u64 emitted = unique < cap ? unique : cap;
+    const u64 mine = C->all[pl.me].unique;
+    const u64 room = cap > before ? cap - before : 0;  // shard-major capacity wall
+    ShardRound& rs = C->rs[r];
+    rs.expanded = E;
+    rs.offered = offered;
+    rs.unique = unique;
+    rs.emitted = emitted;
+    rs.pruned = pruned;
+    rs.routed = routed;
+    rs.overflowed = unique > cap ? 1u : 0u;
+    rs.valid = 1;
+    C->count[(r + 1) & 1] = mine < room ? mine : room;
+    C->round = r + 1;
+    C->epoch = (C->epoch & kEpochMask) == kEpochMask ? 1 : C->epoch + 1;
+    C->ticket = 0;
+    C->mine = ShardStat{};
+    if (emitted == 0 || static_cast<int>(r) + 1 >= pl.rounds) C->stop = 1;
+}
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw DeviceError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// ----------------------------------------------------------------------
+// NCCL, loaded on first use (the product links no NCCL unless sharded)
+
+struct Nccl {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+    static Nccl& get() {
+        static Nccl n;
+        static std::once_flag once;
+        std::call_once(once, [] { n.load(); });
+        if (!n.GetUniqueId) throw DeviceError("NCCL (libnccl.so.2) could not be loaded");
+        return n;
+    }
+    void check(ncclResult_t r, const char* what) const {
+        if (r != ncclSuccess)
+            throw DeviceError(std::string("NCCL error in ") + what + ": " +
+                              (GetErrorString ? GetErrorString(r) : "?"));
+    }
+
+private:
+    void load() {
+        const char* names[] = {std::getenv("ETWG_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+        void* h = nullptr;
+        for (const char* nm : names)
+            if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) return;
+        auto sym = [&](auto& fn, const char* name) { fn = reinterpret_cast<std::decay_t<decltype(fn)>>(dlsym(h, name)); };
+        sym(CommInitRank, "ncclCommInitRank");
+        sym(CommDestroy, "ncclCommDestroy");
+        sym(AllGather, "ncclAllGather");
+        sym(Broadcast, "ncclBroadcast");
+        sym(Send, "ncclSend");
+        sym(Recv, "ncclRecv");
+        sym(GroupStart, "ncclGroupStart");
+        sym(GroupEnd, "ncclGroupEnd");
+        sym(GetErrorString, "ncclGetErrorString");
+        sym(GetUniqueId, "ncclGetUniqueId");
+    }
+};
+
+// ----------------------------------------------------------------------
+// host side
+
+struct Shard {
+    int me = 0;
+    Params* d_params = nullptr;
+    Params* h_params = nullptr;
+    ShardCtl* d_ctl = nullptr;
+    ShardCtl* h_ctl = nullptr;
+    ShardBufs b{};
+    u64 bloom_dirty = 0;  // words of the Bloom slice that may hold bits
+};
+
+class ShardSet {
+public:
+    static ShardSet& instance() {
+        static ShardSet* s = new ShardSet();
+        return *s;
+    }
+    std::mutex mu;
+
+    bool active() const { return G_ > 1; }
+
+    void set_virtual(int G) {
+        if (G < 1 || G > kMaxShards) throw std::invalid_argument("virtual shard count must be 1..8");
+        if (comm_) throw std::invalid_argument("sharding already initialised over NCCL");
+        release();
+        if (G == 1) return;
+        int dev = 0;
+        if (const char* e = std::getenv("ETWG_DEVICE")) dev = std::atoi(e);
+        init_device(dev);
+        G_ = G;
+        local_.resize(G);
+        for (int s = 0; s < G; ++s) create_shard(local_[s], s);
+    }
+
+    void init_nccl(const unsigned char* id, int rank, int world, int device) {
+        if (world < 1 || world > kMaxShards) throw std::invalid_argument("world size must be 1..8");
+        if (rank < 0 || rank >= world) throw std::invalid_argument("rank out of range");
+        release();
+        Nccl& nc = Nccl::get();
+        init_device(device);
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof uid);
+        nc.check(nc.CommInitRank(&comm_, world, uid, rank), "ncclCommInitRank");
+        G_ = world;
+        rank_ = rank;
+        local_.resize(1);
+        create_shard(local_[0], rank);
+    }
+
+    void release() {
+        for (Shard& s : local_) destroy_shard(s);
+        local_.clear();
+        if (comm_) {
+            Nccl::get().CommDestroy(comm_);
+            comm_ = nullptr;
+        }
+        G_ = 1;
+        rank_ = 0;
+    }
+
+    void info(int* world, int* rank, int* virt) const {
+        if (world) *world = G_;
+        if (rank) *rank = rank_;
+        if (virt) *virt = (G_ > 1 && !comm_) ? 1 : 0;
+    }
+
+    void timer_begin() { check(cudaEventRecord(tev_[0], stream_), "timer"); }
+    double timer_end() {
+        check(cudaEventRecord(tev_[1], stream_), "timer");
+        check(cudaEventSynchronize(tev_[1]), "timer sync");
+        float t = 0;
+        check(cudaEventElapsedTime(&t, tev_[0], tev_[1]), "timer elapsed");
+        return t;
+    }
+    // adds this engine's counters to t (engine_times) / clears them
+    void accumulate(KernelTimes& t) const {
+        t.decide_ms += decide_ms_;
+        t.kernel_launches += launches_;
+        t.layer_bytes += layer_bytes_;
+        t.dedup_bytes += dedup_bytes_;
+        t.expanded += expanded_;
+        t.h2d_bytes += h2d_;
+        t.d2h_bytes += d2h_;
+        t.exchange_bytes += exchange_bytes_;
+        t.reruns += reruns_;
+    }
+    void reset_counters() {
+        decide_ms_ = layer_bytes_ = dedup_bytes_ = exchange_bytes_ = 0;
+        launches_ = expanded_ = h2d_ = d2h_ = reruns_ = 0;
+    }
+
+    DecideResult decide(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg, int rounds,
+                        const LayerObserver* observer) {
+        check(cudaSetDevice(device_), "cudaSetDevice");
+        const int n = g.vertex_count();
+        const int W = n > 64 ? 2 : 1;
+        if (rounds < 0) rounds = std::max(0, n - k - 1);
+        if (rounds > kMaxRounds - 1) throw std::invalid_argument("too many rounds");
+        DecideResult res;
+        if (rounds == 0) {
+            res.outcome = Outcome::feasible;
+            return res;
+        }
+        check(cudaEventRecord(ev_[0], stream_), "event");
+        for (Shard& s : local_) setup(s, g, k, forbidden, cfg, rounds);
+        np_floor_ = 1;
+        cap_floor_ = 0;
+        const bool bloom = cfg.dedup == DedupMode::bloom;
+        // host mirror of the global round state
+        std::vector<u64> count(G_, 0);
+        count[0] = 1;  // the root (empty set, history 0xFFFFFFFF) starts on shard 0
+        ShardRound prev{};
+        int r = 0;
+        bool stopped = false;
+        while (r < rounds && !stopped) {
+            const Plan pl = plan(r, count, prev, cfg, W);
+            pl_round_parity_ = r & 1;
+            for (Shard& s : local_) prepare_round(s, pl, W, bloom, count);
+            for (Shard& s : local_) launch_route(s, pl, W, cfg.use_mmw);
+            exchange(pl, W);
+            for (Shard& s : local_) launch_owner(s, pl, W, bloom);
+            allgather_stats();
+            for (Shard& s : local_) {
+                Plan p = pl;
+                p.me = s.me;
+                k_shard_finish<<<1, 32, 0, stream_>>>(s.d_params, s.d_ctl, p);
+                check(cudaGetLastError(), "finish launch");
+                ++launches_;
+            }
+            for (Shard& s : local_) {
+                check(cudaMemcpyAsync(s.h_ctl, s.d_ctl, sizeof(ShardCtl), cudaMemcpyDeviceToHost, stream_),
+                      "control d2h");
+                d2h_ += sizeof(ShardCtl);
+            }
+            check(cudaStreamSynchronize(stream_), "round sync");
+            const ShardCtl& c0 = *local_[0].h_ctl;
+            unsigned abort = 0;
+            u64 need_layer = 0, need_recs = 0, need_parts = 0;
+            for (int s = 0; s < G_; ++s) {
+                abort |= c0.all[s].abort;
+                need_layer = std::max(need_layer, c0.all[s].need_layer);
+                need_recs = std::max(need_recs, c0.all[s].need_recs);
+                need_parts = std::max(need_parts, c0.all[s].need_parts);
+            }
+            if (abort) {
+                if (abort & kAbortRecs) cap_floor_ = std::max(cap_floor_, need_recs);
+                if (abort & kAbortParts) np_floor_ = std::max(np_floor_, need_parts);
+                for (Shard& s : local_) {
+                    if (abort & kAbortLayer) grow_layers(s, need_layer + need_layer / 2, r & 1, count[s.me]);
+                    rearm(s);
+                }
+                ++reruns_;
+                continue;
+            }
+            prev = c0.rs[r];
+            // every shard's kept count, shard-major (as k_shard_finish computed it)
+            const u64 cap = host_round_cap(prev.expanded);
+            u64 before = 0;
+            for (int s = 0; s < G_; ++s) {
+                const u64 u = c0.all[s].unique;
+                const u64 room = cap > before ? cap - before : 0;
+                count[s] = std::min(u, room);
+                before += u;
+            }
+            if (observer) {
+                std::vector<State> layer;
+                for (Shard& s : local_) {
+                    std::vector<State> part = fetch_layer(s, (r + 1) & 1, count[s.me], W);
+                    layer.insert(layer.end(), part.begin(), part.end());
+                }
+                (*observer)(k, r, layer);
+            }
+            stopped = c0.stop != 0;
+            ++r;
+        }
+        const ShardCtl& c0 = *local_[0].h_ctl;
+        bool any_ovf = false;
+        for (int i = 0; i < rounds; ++i) {
+            const ShardRound& s = c0.rs[i];
+            if (!s.valid) break;
+            LayerStats ls;
+            ls.k = k;
+            ls.round = i;
+            ls.expanded = s.expanded;
+            ls.emitted = s.emitted;
+            ls.duplicates = s.offered - s.unique;
+            ls.mmw_pruned = s.pruned;
+            ls.overflowed = s.overflowed != 0;
+            any_ovf = any_ovf || ls.overflowed;
+            res.rounds.push_back(ls);
+            if (s.emitted == 0) break;
+        }
+        res.overflowed = any_ovf;
+        // SURVEY §8d algorithmic bytes (same model as the single-device engine)
+        // plus the records that crossed to other shards
+        const double wb = 8.0 * W + 4.0, db = cfg.dedup == DedupMode::bloom ? 4.0 * cfg.bloom_hashes : 8.0 * W + 8.0;
+        for (int i = 0; i < rounds && c0.rs[i].valid; ++i) {
+            const ShardRound& s = c0.rs[i];
+            layer_bytes_ += wb * static_cast<double>(s.expanded + s.emitted);
+            dedup_bytes_ += db * static_cast<double>(s.offered);
+            expanded_ += s.expanded;
+            exchange_bytes_ += 8.0 * (W + 2) * static_cast<double>(s.routed) * (G_ - 1) / G_;
+        }
+        check(cudaEventRecord(ev_[1], stream_), "event");
+        check(cudaEventSynchronize(ev_[1]), "event sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
+        decide_ms_ += ms;
+        const bool empty = !res.rounds.empty() && res.rounds.back().emitted == 0;
+        if (empty) {
+            res.outcome = any_ovf ? Outcome::indeterminate : Outcome::infeasible;
+            return res;
+        }
+        if (static_cast<int>(res.rounds.size()) != rounds)
+            throw DeviceError("sharded decide stopped early without an empty layer");
+        res.outcome = Outcome::feasible;
+        // witness = front of the final layer on the lowest shard holding states
+        int root = 0;
+        while (root < G_ && count[root] == 0) ++root;
+        res.witness = witness(root, rounds & 1, W);
+        return res;
+    }
+
+private:
+    int G_ = 1, rank_ = 0, device_ = -1;
+    ncclComm_t comm_ = nullptr;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev_[2] = {nullptr, nullptr};
+    std::vector<Shard> local_;
+    u64 np_floor_ = 1, cap_floor_ = 0;
+    u64 free_count_ = 0, max_states_ = 0;
+    double decide_ms_ = 0, layer_bytes_ = 0, dedup_bytes_ = 0, exchange_bytes_ = 0;
+    uint64_t launches_ = 0, reruns_ = 0, expanded_ = 0, h2d_ = 0, d2h_ = 0;
+    cudaEvent_t tev_[2] = {nullptr, nullptr};
+    int grid_route_ = 0, grid_owner_[2] = {0, 0};
+    u64* d_wit_ = nullptr;
+    int pl_round_parity_ = 0;  // buffer holding the current round's input layer
+
+    void init_device(int dev) {
+        if (device_ == dev && stream_) return;
+        check(cudaSetDevice(dev), "cudaSetDevice");
+        device_ = dev;
+        cudaDeviceProp prop;
+        check(cudaGetDeviceProperties(&prop, dev), "device properties");
+        check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+        check(cudaEventCreate(&ev_[0]), "event");
+        check(cudaEventCreate(&ev_[1]), "event");
+        check(cudaEventCreate(&tev_[0]), "event");
+        check(cudaEventCreate(&tev_[1]), "event");
+        check(cudaMalloc(&d_wit_, 32), "witness");
+        auto allow = [&](auto kernel, int bytes, int& grid) {
+            check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem");
+            int blocks = 0;
+            check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kOwnerThreads, bytes), "occupancy");
+            grid = prop.multiProcessorCount * std::max(1, blocks);
+        };
+        allow(k_owner<1, false>, owner_smem_bytes<1>(), grid_owner_[0]);
+        allow(k_owner<1, true>, owner_smem_bytes<1>(), grid_owner_[0]);
+        allow(k_owner<2, false>, owner_smem_bytes<2>(), grid_owner_[1]);
+        allow(k_owner<2, true>, owner_smem_bytes<2>(), grid_owner_[1]);
+        grid_route_ = prop.multiProcessorCount * 4;
+    }
+
+    void create_shard(Shard& s, int me) {
+        s = Shard{};
+        s.me = me;
+        check(cudaMalloc(&s.d_params, sizeof(Params)), "params");
+        check(cudaMallocHost(&s.h_params, sizeof(Params)), "params");
+        check(cudaMalloc(&s.d_ctl, sizeof(ShardCtl)), "control");
+        check(cudaMallocHost(&s.h_ctl, sizeof(ShardCtl)), "control");
+        std::memset(s.h_ctl, 0, sizeof(ShardCtl));
+    }
+
+    static void destroy_shard(Shard& s) {
+        cudaFree(s.d_params);
+        cudaFreeHost(s.h_params);
+        cudaFree(s.d_ctl);
+        cudaFreeHost(s.h_ctl);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(s.b.keys[i]);
+            cudaFree(s.b.hist[i]);
+        }
+        cudaFree(s.b.out);
+        cudaFree(s.b.out_cnt);
+        cudaFree(s.b.in);
+        cudaFree(s.b.in_cnt);
+        cudaFree(s.b.tiles);
+        cudaFree(s.b.bloom);
+        s = Shard{};
+    }
+
+    void setup(Shard& s, const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg, int rounds) {
+        Params& p = *s.h_params;
+        std::memset(&p, 0, sizeof p);
+        p.n = g.vertex_count();
+        p.k = k;
+        p.rounds = rounds;
+        p.free_count = std::max(0, g.vertex_count() - forbidden.count());
+        p.hashes = cfg.bloom_hashes;
+        p.bpe = cfg.bloom_bits_per_element;
+        p.max_states = cfg.max_layer_states;
+        p.forbidden[0] = forbidden.w[0];
+        p.forbidden[1] = forbidden.w[1];
+        for (int v = 0; v < g.vertex_count(); ++v) {
+            p.rows[v][0] = g.neighbors(v).w[0];
+            p.rows[v][1] = g.neighbors(v).w[1];
+        }
+        free_count_ = static_cast<u64>(p.free_count);
+        max_states_ = p.max_states;
+        check(cudaMemcpyAsync(s.d_params, s.h_params, sizeof(Params), cudaMemcpyHostToDevice, stream_), "params");
+        h2d_ += sizeof(Params) + sizeof(ShardCtl);
+        ShardCtl& c = *s.h_ctl;
+        const unsigned epoch = c.epoch;
+        std::memset(&c, 0, sizeof c);
+        c.epoch = next_epoch(s, epoch);
+        c.count[0] = s.me == 0 ? 1 : 0;
+        check(cudaMemcpyAsync(s.d_ctl, s.h_ctl, sizeof(ShardCtl), cudaMemcpyHostToDevice, stream_), "control");
+        grow_layers(s, 1 << 16, 0, 0);
+        if (s.me == 0) {
+            const u64 zero2[2] = {0, 0};
+            const unsigned root_hist = 0xFFFFFFFFu;
+            check(cudaMemcpyAsync(s.b.keys[0], zero2, 16, cudaMemcpyHostToDevice, stream_), "root");
+            check(cudaMemcpyAsync(s.b.hist[0], &root_hist, 4, cudaMemcpyHostToDevice, stream_), "root");
+            check(cudaStreamSynchronize(stream_), "root");
+        }
+    }
+
+    unsigned next_epoch(Shard& s, unsigned e) {
+        e = (e + 1) & kEpochMask;
+        if (e == 0) {
+            e = 1;
+            if (s.b.tiles) check(cudaMemsetAsync(s.b.tiles, 0, s.b.tile_cap * 8, stream_), "tiles clear");
+        }
+        return e;
+    }
+
+    u64 host_round_cap(u64 e_in) const {
+        u64 upper = e_in * free_count_;
+        if (upper < 1) upper = 1;
+        return std::min<u64>(max_states_, upper);
+    }
+
+    static u64 pow2_at_least(u64 x) {
+        u64 s = 1;
+        while (s < x) s <<= 1;
+        return s;
+    }
+
+    Plan plan(int r, const std::vector<u64>& count, const ShardRound& prev, const DpConfig& cfg, int W) {
+        u64 E = 0, Emax = 0;
+        for (u64 c : count) {
+            E += c;
+            Emax = std::max(Emax, c);
+        }
+        const u64 fc = std::max<u64>(free_count_, 1);
+        u64 distinct = std::max<u64>(E * fc, 1), routed_max = std::max<u64>(Emax * fc, 1);
+        if (r > 0 && prev.expanded) {
+            const double grow_u = static_cast<double>(prev.unique) / static_cast<double>(prev.expanded);
+            const double grow_r = static_cast<double>(prev.routed) / static_cast<double>(prev.expanded);
+            distinct = std::min<u64>(distinct, static_cast<u64>(static_cast<double>(E) * grow_u * 1.25) + 64);
+            routed_max = std::min<u64>(routed_max, static_cast<u64>(static_cast<double>(Emax) * grow_r * 1.25) + 64);
+        }
+        Plan pl{};
+        pl.G = G_;
+        pl.rounds = local_[0].h_params->rounds;
+        const u64 per_owner = (distinct + G_ - 1) / G_;
+        pl.np = std::max<u64>(pow2_at_least((per_owner + owner_target<1>() - 1) / owner_target<1>()), np_floor_);
+        pl.lg = 0;
+        while ((u64{1} << pl.lg) < pl.np) ++pl.lg;
+        const u64 per = (routed_max + G_ * pl.np - 1) / (G_ * pl.np);
+        pl.cap = std::max<u64>(per + per / 4 + 64, cap_floor_);
+        pl.layer_est = per_owner + per_owner / 4 + 1024;
+        pl.bloom_m = 0;
+        if (cfg.dedup == DedupMode::bloom) {
+            const u64 cap = host_round_cap(E);
+            pl.bloom_m = bloom_bits_for((cap + G_ - 1) / G_, cfg.bloom_bits_per_element);
+        }
+        (void)W;
+        return pl;
+    }
+
+    void grow_layers(Shard& s, u64 states, int keep_buf, u64 keep_count) {
+        if (states <= s.b.layer_cap && s.b.keys[0]) return;
+        const u64 cap = std::max<u64>(states, std::max<u64>(s.b.layer_cap * 2, u64{1} << 16));
+        u64* keys[2];
+        unsigned* hist[2];
+        for (int i = 0; i < 2; ++i) {
+            check(cudaMalloc(&keys[i], cap * 16), "layer keys");
+            check(cudaMalloc(&hist[i], cap * 4), "layer hist");
+        }
+        if (s.b.keys[0] && keep_count) {
+            check(cudaMemcpyAsync(keys[keep_buf], s.b.keys[keep_buf], keep_count * 16, cudaMemcpyDeviceToDevice, stream_),
+                  "keep layer");
+            check(cudaMemcpyAsync(hist[keep_buf], s.b.hist[keep_buf], keep_count * 4, cudaMemcpyDeviceToDevice, stream_),
+                  "keep layer");
+        }
+        check(cudaStreamSynchronize(stream_), "sync");
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(s.b.keys[i]);
+            cudaFree(s.b.hist[i]);
+            s.b.keys[i] = keys[i];
+            s.b.hist[i] = hist[i];
+        }
+        s.b.layer_cap = cap;
+    }
+
+    void prepare_round(Shard& s, const Plan& pl, int W, bool bloom, const std::vector<u64>& count) {
+        const u64 recs = static_cast<u64>(G_) * pl.np * pl.cap;
+        const u64 cnts = static_cast<u64>(G_) * pl.np;
+        if (recs > s.b.box_cap || !s.b.out) {
+            const u64 cap = std::max<u64>(recs + recs / 4, u64{1} << 16);
+            cudaFree(s.b.out);
+            cudaFree(s.b.in);
+            check(cudaMalloc(&s.b.out, cap * 32), "outbox");
+            check(cudaMalloc(&s.b.in, cap * 32), "inbox");
+            s.b.box_cap = cap;
+        }
+        if (cnts > s.b.cnt_cap || !s.b.out_cnt) {
+            const u64 cap = std::max<u64>(cnts * 2, u64{1} << 12);
+            cudaFree(s.b.out_cnt);
+            cudaFree(s.b.in_cnt);
+            check(cudaMalloc(&s.b.out_cnt, cap * 4), "outbox counts");
+            check(cudaMalloc(&s.b.in_cnt, cap * 4), "inbox counts");
+            s.b.cnt_cap = cap;
+        }
+        if (pl.np + 1 > s.b.tile_cap || !s.b.tiles) {
+            const u64 cap = std::max<u64>((pl.np + 1) * 2, u64{1} << 12);
+            cudaFree(s.b.tiles);
+            check(cudaMalloc(&s.b.tiles, cap * 8), "tiles");
+            check(cudaMemsetAsync(s.b.tiles, 0, cap * 8, stream_), "tiles");
+            s.b.tile_cap = cap;
+        }
+        // the next layer holds about this shard's share of the distinct keys
+        grow_layers(s, pl.layer_est, pl_round_parity_, count[s.me]);
+        check(cudaMemsetAsync(s.b.out_cnt, 0, cnts * 4, stream_), "outbox counts");
+        if (bloom) {
+            const u64 words = (pl.bloom_m + 31) / 32;
+            if (words > s.b.bloom_cap || !s.b.bloom) {
+                const u64 cap = std::max<u64>(words + words / 4, u64{1} << 20);
+                cudaFree(s.b.bloom);
+                check(cudaMalloc(&s.b.bloom, cap * 4), "bloom slice");
+                s.b.bloom_cap = cap;
+                s.bloom_dirty = cap;
+            }
+            // a fresh filter every round (dp.cpp:93-94)
+            const u64 clear = std::min(std::max(s.bloom_dirty, words), s.b.bloom_cap);
+            check(cudaMemsetAsync(s.b.bloom, 0, clear * 4, stream_), "bloom clear");
+            s.bloom_dirty = words;
+        }
+        (void)W;
+    }
+
+    void launch_route(Shard& s, const Plan& pl, int W, bool mmw) {
+        Plan p = pl;
+        p.me = s.me;
+        if (W == 1) {
+            if (mmw) k_route<1, true><<<grid_route_, kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
+            else k_route<1, false><<<grid_route_, kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
+        } else {
+            if (mmw) k_route<2, true><<<grid_route_, kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
+            else k_route<2, false><<<grid_route_, kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
+        }
+        check(cudaGetLastError(), "route launch");
+        ++launches_;
+    }
+
+    void launch_owner(Shard& s, const Plan& pl, int W, bool bloom) {
+        Plan p = pl;
+        p.me = s.me;
+        if (W == 1) {
+            if (bloom) k_owner<1, true><<<grid_owner_[0], kOwnerThreads, owner_smem_bytes<1>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
+            else k_owner<1, false><<<grid_owner_[0], kOwnerThreads, owner_smem_bytes<1>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
+        } else {
+            if (bloom) k_owner<2, true><<<grid_owner_[1], kOwnerThreads, owner_smem_bytes<2>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
+            else k_owner<2, false><<<grid_owner_[1], kOwnerThreads, owner_smem_bytes<2>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
+        }
+        check(cudaGetLastError(), "owner launch");
+        ++launches_;
+    }
+
+    // outbox block d of shard s -> inbox slot s of shard d
+    void exchange(const Plan& pl, int W) {
+        const u64 rec_bytes = 8ull * (W + 2);
+        const u64 block = pl.np * pl.cap;
+        const u64 bytes = block * rec_bytes, cnt_bytes = pl.np * 4;
+        if (!comm_) {
+            for (Shard& src : local_)
+                for (Shard& dst : local_) {
+                    check(cudaMemcpyAsync(dst.b.in + src.me * block * (W + 2), src.b.out + dst.me * block * (W + 2),
+                                          bytes, cudaMemcpyDeviceToDevice, stream_), "exchange");
+                    check(cudaMemcpyAsync(dst.b.in_cnt + src.me * pl.np, src.b.out_cnt + dst.me * pl.np, cnt_bytes,
+                                          cudaMemcpyDeviceToDevice, stream_), "exchange counts");
+                }
+            return;
+        }
+        Nccl& nc = Nccl::get();
+        Shard& s = local_[0];
+        nc.check(nc.GroupStart(), "group start");
+        for (int d = 0; d < G_; ++d) {
+            if (d == s.me) continue;
+            nc.check(nc.Send(s.b.out + d * block * (W + 2), bytes, ncclUint8, d, comm_, stream_), "send");
+            nc.check(nc.Recv(s.b.in + d * block * (W + 2), bytes, ncclUint8, d, comm_, stream_), "recv");
+            nc.check(nc.Send(s.b.out_cnt + d * pl.np, cnt_bytes, ncclUint8, d, comm_, stream_), "send counts");
+            nc.check(nc.Recv(s.b.in_cnt + d * pl.np, cnt_bytes, ncclUint8, d, comm_, stream_), "recv counts");
+        }
+        nc.check(nc.GroupEnd(), "group end");
+        check(cudaMemcpyAsync(s.b.in + s.me * block * (W + 2), s.b.out + s.me * block * (W + 2), bytes,
+                              cudaMemcpyDeviceToDevice, stream_), "self exchange");
+        check(cudaMemcpyAsync(s.b.in_cnt + s.me * pl.np, s.b.out_cnt + s.me * pl.np, cnt_bytes,
+                              cudaMemcpyDeviceToDevice, stream_), "self exchange counts");
+    }
+
+    void allgather_stats() {
+        if (!comm_) {
+            for (Shard& src : local_)
+                for (Shard& dst : local_)
+                    check(cudaMemcpyAsync(&dst.d_ctl->all[src.me], &src.d_ctl->mine, sizeof(ShardStat),
+                                          cudaMemcpyDeviceToDevice, stream_), "stat gather");
+            return;
+        }
+        Nccl& nc = Nccl::get();
+        Shard& s = local_[0];
+        nc.check(nc.AllGather(&s.d_ctl->mine, &s.d_ctl->all[0], sizeof(ShardStat), ncclUint8, comm_, stream_),
+                 "allgather stats");
+    }
+
+    // re-arm an aborted round: counters cleared, new look-back epoch
+    void rearm(Shard& s) {
+        ShardCtl& c = *s.h_ctl;
+        c.ticket = 0;
+        c.mine = ShardStat{};
+        c.epoch = next_epoch(s, c.epoch);
+        check(cudaMemcpyAsync(s.d_ctl, s.h_ctl, offsetof(ShardCtl, all), cudaMemcpyHostToDevice, stream_), "re-arm");
+    }
+
+    std::vector<State> fetch_layer(Shard& s, int buf, u64 count, int W) {
+        std::vector<u64> keys(static_cast<size_t>(W) * count);
+        std::vector<unsigned> hist(count);
+        if (count) {
+            check(cudaMemcpyAsync(keys.data(), s.b.keys[buf], keys.size() * 8, cudaMemcpyDeviceToHost, stream_), "layer");
+            check(cudaMemcpyAsync(hist.data(), s.b.hist[buf], count * 4, cudaMemcpyDeviceToHost, stream_), "layer");
+            check(cudaStreamSynchronize(stream_), "sync");
+        }
+        std::vector<State> out(count);
+        for (u64 i = 0; i < count; ++i) {
+            out[i].set.w[0] = keys[W * i];
+            out[i].set.w[1] = W == 2 ? keys[W * i + 1] : 0;
+            out[i].history = hist[i];
+        }
+        return out;
+    }
+
+    State witness(int root, int buf, int W) {
+        u64 h[4] = {0, 0, 0, 0};
+        if (!comm_) {
+            Shard& s = local_[root];
+            check(cudaMemcpyAsync(h, s.b.keys[buf], 8 * W, cudaMemcpyDeviceToHost, stream_), "witness");
+            check(cudaMemcpyAsync(&h[2], s.b.hist[buf], 4, cudaMemcpyDeviceToHost, stream_), "witness");
+        } else {
+            Shard& s = local_[0];
+            if (s.me == root) {
+                check(cudaMemcpyAsync(d_wit_, s.b.keys[buf], 8 * W, cudaMemcpyDeviceToDevice, stream_), "witness");
+                check(cudaMemcpyAsync(d_wit_ + 2, s.b.hist[buf], 4, cudaMemcpyDeviceToDevice, stream_), "witness");
+            }
+            Nccl& nc = Nccl::get();
+            nc.check(nc.Broadcast(d_wit_, d_wit_, 24, ncclUint8, root, comm_, stream_), "broadcast witness");
+            check(cudaMemcpyAsync(h, d_wit_, 24, cudaMemcpyDeviceToHost, stream_), "witness");
+        }
+        check(cudaStreamSynchronize(stream_), "sync");
+        State st;
+        st.set.w[0] = h[0];
+        st.set.w[1] = W == 2 ? h[1] : 0;
+        st.history = static_cast<uint32_t>(h[2]);
+        return st;
+    }
+};
+
+}  // namespace
+
+bool shard_active() {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    return s.active();
+}
+
+DecideResult shard_decide(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg, int rounds,
+                          const LayerObserver* observer) {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    return s.decide(g, k, forbidden, cfg, rounds, observer);
+}
+
+void shard_set_virtual(int G) {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.set_virtual(G);
+}
+
+void shard_unique_id(unsigned char* out128) {
+    Nccl& nc = Nccl::get();
+    ncclUniqueId id;
+    nc.check(nc.GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, sizeof id);
+}
+
+void shard_init_nccl(const unsigned char* id128, int rank, int world, int device) {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.init_nccl(id128, rank, world, device);
+}
+
+void shard_release() {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.release();
+}
+
+void shard_info(int* world, int* rank, int* virt) {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.info(world, rank, virt);
+}
+
+void shard_timer_begin() {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.timer_begin();
+}
+
+double shard_timer_end() {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    return s.timer_end();
+}
+
+void shard_accumulate(KernelTimes& t) {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.accumulate(t);
+}
+
+void shard_reset_times() {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.reset_counters();
+}
+
+}  // namespace etw

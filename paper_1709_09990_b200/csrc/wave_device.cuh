@@ -406,6 +406,42 @@ __device__ __forceinline__ u64 child_rank(u64 parent_idx, int v) {
     return parent_idx * (64 * W) + static_cast<u64>(v);  // dp.cpp:66 (idx*64+v)
 }
 
+// Shared-memory open-addressing claim: the slot at `keys + W*h` becomes
+// `key` if it was empty (0); true when the slot now holds `key`.
+template <int W>
+__device__ __forceinline__ bool smem_claim(u64* keys, unsigned h, const Set<W>& key) {
+    if constexpr (W == 1) {
+        const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(keys + h), 0ull, key.w[0]);
+        return prev == 0 || prev == key.w[0];
+    } else {
+        u64 lo, hi;
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(keys + 2 * h));
+        asm volatile(
+            "{\n\t.reg .b128 c, s, d;\n\t"
+            "mov.b128 c, {%2, %3};\n\t"
+            "mov.b128 s, {%4, %5};\n\t"
+            "atom.shared.cas.b128 d, [%6], c, s;\n\t"
+            "mov.b128 {%0, %1}, d;\n\t}"
+            : "=l"(lo), "=l"(hi)
+            : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
+            : "memory");
+        return (lo | hi) == 0 || (lo == key.w[0] && hi == key.w[1]);
+    }
+}
+
+// Shared-memory lookup after all claims: slot of `key` or -1.
+template <int W>
+__device__ __forceinline__ int smem_find(const u64* keys, unsigned h, unsigned mask, const Set<W>& key,
+                                         int max_probes) {
+    for (int probe = 0; probe < max_probes; ++probe) {
+        bool hit = keys[W * h] == key.w[0];
+        if constexpr (W == 2) hit = hit && keys[2 * h + 1] == key.w[1];
+        if (hit) return static_cast<int>(h);
+        h = (h + 1) & mask;
+    }
+    return -1;
+}
+
 // ----------------------------------------------------------------------
 // CTA-scope duplicate filter. A tile of consecutive parents (siblings of the
 // same grandparents sit next to each other in a rank-ordered layer) offers

@@ -1196,6 +1196,7 @@ DecideResult device_decide(const Graph& g, int k, const HostSet& forbidden, cons
                            int rounds, const LayerObserver* observer) {
     if (k < 0) throw std::invalid_argument("k must be non-negative");
     if (cfg.max_layer_states == 0) throw std::invalid_argument("layer capacity must be positive");
+    if (shard_active()) return shard_decide(g, k, forbidden, cfg, rounds, observer);
     Engine& e = Engine::instance();
     std::lock_guard<std::mutex> lock(e.mu);
     return e.decide(g, k, forbidden, cfg, rounds, observer);
@@ -1226,12 +1227,14 @@ bool device_available(DeviceInfo* info) {
 }
 
 void engine_timer_begin() {
+    if (shard_active()) return shard_timer_begin();
     Engine& e = Engine::instance();
     std::lock_guard<std::mutex> lock(e.mu);
     e.timer_begin();
 }
 
 double engine_timer_end() {
+    if (shard_active()) return shard_timer_end();
     Engine& e = Engine::instance();
     std::lock_guard<std::mutex> lock(e.mu);
     return e.timer_end();
@@ -1244,15 +1247,23 @@ void engine_set_profiling(bool on) {
 }
 
 KernelTimes engine_times() {
-    Engine& e = Engine::instance();
-    std::lock_guard<std::mutex> lock(e.mu);
-    return e.prof.t;
+    KernelTimes t;
+    {
+        Engine& e = Engine::instance();
+        std::lock_guard<std::mutex> lock(e.mu);
+        t = e.prof.t;
+    }
+    shard_accumulate(t);
+    return t;
 }
 
 void engine_reset_times() {
-    Engine& e = Engine::instance();
-    std::lock_guard<std::mutex> lock(e.mu);
-    e.prof.t = KernelTimes{};
+    {
+        Engine& e = Engine::instance();
+        std::lock_guard<std::mutex> lock(e.mu);
+        e.prof.t = KernelTimes{};
+    }
+    shard_reset_times();
 }
 
 }  // namespace etw

@@ -117,6 +117,11 @@ def library() -> C.CDLL:
         "etwg_improve_graph": (None, [C.c_int, _u64p, C.c_int, _u64p]),
         "etwg_mmw_lower_bound": (C.c_int, [C.c_int, _u64p, _u64p, C.c_int]),
         "etwg_split": (C.c_int, [C.c_int, _u64p, C.c_int, _ip, _ip, _ip]),
+        "etwg_set_virtual_shards": (C.c_int, [C.c_int, C.c_char_p, C.c_size_t]),
+        "etwg_nccl_unique_id": (C.c_int, [_u8p, C.c_char_p, C.c_size_t]),
+        "etwg_shard_init": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
+        "etwg_shard_release": (None, []),
+        "etwg_shard_info": (None, [_ip, _ip, _ip]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -436,13 +441,53 @@ def reset_times() -> None:
 TIME_KEYS = ("decide_ms", "expand_ms", "insert_ms", "append_ms", "clear_ms", "fused_ms",
              "expand_launches", "insert_launches", "append_launches", "clear_launches",
              "fused_launches", "kernel_launches", "layer_bytes", "dedup_bytes", "expanded",
-             "h2d_bytes", "d2h_bytes")
+             "h2d_bytes", "d2h_bytes", "exchange_bytes", "reruns")
 
 
 def times() -> dict:
     buf = (C.c_double * len(TIME_KEYS))()
     n = library().etwg_times(buf, len(TIME_KEYS))
     return {TIME_KEYS[i]: buf[i] for i in range(n)}
+
+
+# owner sharding (include/elimtw_gpu.h)
+
+def set_virtual_shards(shards: int) -> None:
+    """G virtual shards on this process's device (1 turns sharding off)."""
+    err = C.create_string_buffer(1024)
+    st = library().etwg_set_virtual_shards(shards, err, 1024)
+    if st != ETW_OK:
+        _raise(st, err)
+
+
+def nccl_unique_id() -> bytes:
+    out = (C.c_uint8 * 128)()
+    err = C.create_string_buffer(1024)
+    st = library().etwg_nccl_unique_id(out, err, 1024)
+    if st != ETW_OK:
+        _raise(st, err)
+    return bytes(out)
+
+
+def shard_init(uid: bytes, rank: int, world: int, device: int) -> None:
+    """This process becomes shard `rank` of `world` over NCCL on `device`."""
+    if len(uid) != 128:
+        raise ValueError("ncclUniqueId must be 128 bytes")
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    err = C.create_string_buffer(1024)
+    st = library().etwg_shard_init(buf, rank, world, device, err, 1024)
+    if st != ETW_OK:
+        _raise(st, err)
+
+
+def shard_release() -> None:
+    library().etwg_shard_release()
+
+
+def shard_info() -> dict:
+    w, r, v = C.c_int(), C.c_int(), C.c_int()
+    library().etwg_shard_info(C.byref(w), C.byref(r), C.byref(v))
+    return {"world": w.value, "rank": r.value, "virtual": bool(v.value)}
 
 
 # host preprocessing (no device needed)

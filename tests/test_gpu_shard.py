@@ -1,0 +1,161 @@
+"""Owner-sharded decides on one B200 through G virtual shards:
+the same route / exchange / owner / allgather / finish sequence the NCCL path
+runs with one shard per GPU, with the exchange done as device copies. Exact
+mode must give, for every G, the single-device engine's per-round counters
+(expanded, emitted, duplicates, mmw_pruned, overflow) and per-round state
+SETS (north_star: "per-level unique-state counts and the sorted state sets
+must also match"); Bloom mode the same verdicts with layers that are subsets
+of the exact layers."""
+import json
+
+import pytest
+
+from conftest import instance_text
+from paper_1709_09990_b200 import generators as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def shards(E, gpu):
+    def use(g):
+        E.set_virtual_shards(g)
+        return g
+    yield use
+    E.set_virtual_shards(1)
+
+
+def _sets(run):
+    return [sorted(s for s, _ in layer) for layer in run.layers]
+
+
+def _counters(run):
+    return [x.tuple() for x in run.rounds]
+
+
+def _check_witness(rows, k, run):
+    """A feasible run's witness is a state of the final layer."""
+    if run.outcome == "feasible" and run.layers:
+        assert (run.witness_set, run.witness_hist) in set(run.layers[-1])
+
+
+CASES = [
+    ("myciel4", G.myciel(4), 9),
+    ("myciel4", G.myciel(4), 10),
+    ("queen5_5", None, 17),
+    ("g30", G.random_graph(7, 30, 0.25), 9),
+    ("g40", G.random_graph(1, 40, 0.3), 21),
+    ("g40", G.random_graph(1, 40, 0.3), 22),
+]
+
+
+def _rows(name, rows):
+    if rows is not None:
+        return rows
+    from paper_1709_09990_b200 import elimtw
+    return elimtw.Graph.parse(instance_text(name)).rows()
+
+
+@pytest.mark.parametrize("g", [2, 3, 8])
+def test_sharded_exact_matches_single_device(E, shards, g):
+    base = {}
+    for name, rows, k in CASES:
+        rows = _rows(name, rows)
+        base[(name, k)] = E.decide(rows, k, dedup="exact")
+    shards(g)
+    for name, rows, k in CASES:
+        rows = _rows(name, rows)
+        got = E.decide(rows, k, dedup="exact")
+        want = base[(name, k)]
+        assert got.outcome == want.outcome, (name, k, g)
+        assert _counters(got) == _counters(want), (name, k, g)
+        assert _sets(got) == _sets(want), (name, k, g)
+        _check_witness(rows, k, got)
+
+
+def test_sharded_histories_are_min_rank_emissions(E, shards):
+    """Every state's history names its last four eliminations: the low byte
+    is a member of the set and each byte is a vertex of it (or 0xFF)."""
+    rows = G.random_graph(1, 40, 0.3)
+    shards(4)
+    run = E.decide(rows, 21, dedup="exact")
+    for r, layer in enumerate(run.layers):
+        for s, h in layer:
+            for b in range(min(4, r + 1)):
+                v = (h >> (8 * b)) & 0xFF
+                assert s >> v & 1, (r, hex(s), hex(h))
+
+
+def test_sharded_deterministic_for_fixed_g(E, shards):
+    rows = G.random_graph(2, 36, 0.3)
+    shards(4)
+    a = E.decide(rows, 18, dedup="exact")
+    b = E.decide(rows, 18, dedup="exact")
+    assert a.layers == b.layers and (a.witness_set, a.witness_hist) == (b.witness_set, b.witness_hist)
+
+
+def test_sharded_mmw_counters(E, shards):
+    rows = E.Graph.parse(instance_text("queen5_5")).rows()
+    want = E.decide(rows, 18, dedup="exact", mmw=True)
+    shards(2)
+    got = E.decide(rows, 18, dedup="exact", mmw=True)
+    assert _counters(got) == _counters(want)
+    assert _sets(got) == _sets(want)
+
+
+def test_sharded_capacity_wall(E, shards):
+    """Truncation keeps min(unique, cap) states (dp.cpp:152-155) shard-major."""
+    rows = G.random_graph(1, 40, 0.3)
+    want = E.decide(rows, 22, dedup="exact", cap=20_000)
+    shards(4)
+    got = E.decide(rows, 22, dedup="exact", cap=20_000)
+    assert [x.emitted for x in got.rounds[:6]] == [x.emitted for x in want.rounds[:6]]
+    assert got.overflowed == want.overflowed
+    for (a, b) in zip(got.rounds, want.rounds):
+        if not b.overflowed:
+            continue
+        assert a.emitted == b.emitted == 20_000
+
+
+def test_sharded_bloom_subset_of_exact(E, shards):
+    rows = G.random_graph(1, 40, 0.3)
+    shards(4)
+    for k in (21, 22):
+        ex = E.decide(rows, k, dedup="exact")
+        bl = E.decide(rows, k, dedup="bloom")
+        assert bl.outcome == ex.outcome
+        # round by round the Bloom layer (from its own parents) is a subset of
+        # the exact expansion of those parents: check it on the first layers,
+        # where both runs have the same parents unless a false positive hit
+        for r in range(len(bl.layers)):
+            if _sets(bl)[r] != _sets(ex)[r]:
+                assert set(_sets(bl)[r]) <= set(_sets(ex)[r])
+                break
+
+
+def test_sharded_128bit_path(E, oracle, shards):
+    """n > 64: 16-byte keys through route / owner (oracle is the checker)."""
+    cases = [(G.random_graph(i + 7, n, 8.0 / n), 5, 6, False) for i, n in ((1, 72), (3, 96), (5, 128))]
+    cases.append((G.grid_with_chords(8, 9, 6, 7), 4, 6, True))
+    want = [oracle.decide(rows, k, dedup="exact", rounds=rounds, mmw=mmw) for rows, k, rounds, mmw in cases]
+    shards(3)
+    for (rows, k, rounds, mmw), b in zip(cases, want):
+        a = E.decide(rows, k, dedup="exact", rounds=rounds, mmw=mmw)
+        assert a.outcome == b.outcome
+        assert _counters(a) == _counters(b)
+        assert _sets(a) == _sets(b)
+
+
+def test_sharded_solve_stats_identical(E, shards):
+    """etw_solve through the unchanged C API: the stats JSON (every layer
+    counter of every attempt) equals the single-device solve's in exact mode,
+    and the reconstructed order validates to the treewidth."""
+    g = E.Graph.from_rows(G.random_graph(1, 40, 0.3))
+    want = E.solve(g, E.Options(dedup="exact"))
+    shards(8)
+    got = E.solve(g, E.Options(dedup="exact"))
+    assert got.value == want.value == 22
+    assert json.loads(got.stats_json) == json.loads(want.stats_json)
+    res = E.solve(g, E.Options(dedup="exact", emit_order=True))
+    width, valid = g.check_order(res.order)
+    assert res.value == 22 and valid and width <= 22
