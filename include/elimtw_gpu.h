@@ -73,8 +73,8 @@ ELIMTW_API uint64_t etwg_bloom_insert(uint64_t expected, int bits_per_element, i
  * out[0..] = decide_ms, expand_ms, insert_ms, append_ms, clear_ms, fused_ms,
  * expand_launches, insert_launches, append_launches, clear_launches,
  * fused_launches, kernel_launches, layer_bytes, dedup_bytes, expanded,
- * h2d_bytes, d2h_bytes, exchange_bytes, reruns. Returns the number of values
- * written. */
+ * h2d_bytes, d2h_bytes, exchange_bytes, reruns, expand_bytes, insert_bytes,
+ * append_bytes, offered, unique. Returns the number of values written. */
 ELIMTW_API int etwg_times(double* out, int len);
 /* CUDA events on the engine stream around a region; end synchronizes and
  * returns the device milliseconds in between. */

@@ -423,7 +423,12 @@ int etwg_times(double* out, int len) {
                         static_cast<double>(t.h2d_bytes),
                         static_cast<double>(t.d2h_bytes),
                         t.exchange_bytes,
-                        static_cast<double>(t.reruns)};
+                        static_cast<double>(t.reruns),
+                        t.expand_bytes,
+                        t.insert_bytes,
+                        t.append_bytes,
+                        static_cast<double>(t.offered),
+                        static_cast<double>(t.unique)};
     int n = static_cast<int>(sizeof v / sizeof v[0]);
     if (len < n) n = len;
     for (int i = 0; i < n; ++i) out[i] = v[i];

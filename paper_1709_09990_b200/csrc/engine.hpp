@@ -105,6 +105,10 @@ struct KernelTimes {
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of the engine
     double exchange_bytes = 0;  // sharded: child records sent to other shards
     uint64_t reruns = 0;        // sharded: rounds re-run after a buffer grew
+    // per-kernel-class algorithmic bytes: expand / scatter,
+    // insert / partition dedup, append
+    double expand_bytes = 0, insert_bytes = 0, append_bytes = 0;
+    uint64_t offered = 0, unique = 0;  // children offered to dedup / distinct children
 };
 // Brackets a region on the engine's stream with CUDA events; end returns the
 // device milliseconds between the two events (synchronizing).

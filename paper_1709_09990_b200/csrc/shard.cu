@@ -40,6 +40,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <numeric>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -107,6 +108,11 @@ struct ShardBufs {
     unsigned* in_cnt;    // [source][partition]
     u64 box_cap;         // records per box
     u64 cnt_cap;         // counters per box
+    // where the owner reads source s's records for it: the inbox block the
+    // exchange filled (NCCL), or source s's own outbox block (virtual shards
+    // of one device, and a shard's records for itself — no copy)
+    const u64* src_recs[kMaxShards];
+    const unsigned* src_cnt[kMaxShards];
     u64* tiles;          // look-back status per partition
     u64 tile_cap;
     unsigned* bloom;     // the owner's Bloom slice (32-bit words)
@@ -130,34 +136,52 @@ __device__ __forceinline__ u64 part_hash_bits(const Set<W>& key, int lg) {
 // ----------------------------------------------------------------------
 // k_route: candidates of the local parents, children to owner buckets
 
-template <int W, bool MMW>
+template <int W>
+constexpr int route_tile_slots() { return W == 1 ? 4096 : 2048; }
+template <int W>
+constexpr int route_smem_bytes() { return static_cast<int>(sizeof(TileSet<W, route_tile_slots<W>()>)); }
+
+// TILE: identical children of one tile of 256 consecutive parents are
+// resolved in shared memory first (tile_dedup keeps the minimum emission
+// rank, so the owner's min-rank choice is unchanged) — fewer records cross
+// NVLink at the cost of two shared-memory passes per child.
+template <int W, bool MMW, bool TILE>
 __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restrict__ P, ShardCtl* C,
                                                          ShardBufs B, Plan pl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& ts = *reinterpret_cast<TileSet<W, route_tile_slots<W>()>*>(smem_raw);
     __shared__ Set<W> adj[64 * W];
+    __shared__ unsigned win[kRouteThreads][2 * W];
     if (C->stop) return;
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) C->mine.expanded = E;
     load_adjacency<W>(P, adj);
-    __syncthreads();
     const int lane = threadIdx.x & 31;
     const Set<W> forbidden = param_set<W>(P->forbidden);
     const u64* in = B.keys[r & 1];
     const unsigned* hin = B.hist[r & 1];
-    const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-    const u64 nwarps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     const u64 src_tag = static_cast<u64>(pl.me) << 40;
-    u64 offered = 0, pruned = 0;
+    const u64 ntiles = (E + kRouteThreads - 1) / kRouteThreads;
+    u64 offered = 0, pruned = 0, routed = 0;
     bool full = false;
-    for (u64 base = (gtid >> 5) * 32; base < E; base += nwarps * 32) {
-        const u64 idx = base + lane;
+    __syncthreads();
+    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const u64 idx = tile * kRouteThreads + threadIdx.x;
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
         const unsigned H = valid ? hin[idx] : 0u;
-        const Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
+        Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
         offered += M.count();
+        if constexpr (TILE) {
+            tile_set_clear<W, route_tile_slots<W>()>(ts);
+            __syncthreads();
+            tile_dedup<W, route_tile_slots<W>()>(ts, win, S, M);
+        }
+        routed += M.count();
         WarpFlat f;
         f.scan(M.count());
+        const u64 warp_base = tile * kRouteThreads + (threadIdx.x & ~31);
         for (int t = 0; t < f.total; t += 32) {
             const int j = t + lane;
             const int src = f.source(j);
@@ -175,25 +199,25 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
                     u64* rec = B.out + (bucket * pl.cap + slot) * srec_words<W>();
 #pragma unroll
                     for (int w = 0; w < W; ++w) rec[w] = key.w[w];
-                    rec[W] = src_tag | child_rank<W>(base + src, v);
+                    rec[W] = src_tag | child_rank<W>(warp_base + src, v);
                     rec[W + 1] = (static_cast<u64>(Hs) << 8) | static_cast<u64>(v & 0xFF);  // push_history
                 } else {
                     full = true;
                 }
             }
         }
+        if constexpr (TILE) __syncthreads();  // the next tile clears the tile set
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         offered += __shfl_xor_sync(kFull, offered, o);
         pruned += __shfl_xor_sync(kFull, pruned, o);
+        routed += __shfl_xor_sync(kFull, routed, o);
     }
     full = __any_sync(kFull, full);
     if (lane == 0) {
-        if (offered) {
-            atomicAdd(&C->mine.offered, offered);
-            atomicAdd(&C->mine.routed, offered);
-        }
+        if (offered) atomicAdd(&C->mine.offered, offered);
+        if (routed) atomicAdd(&C->mine.routed, routed);
         if (pruned) atomicAdd(&C->mine.pruned, pruned);
         if (full) {
             atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortRecs));
@@ -248,9 +272,8 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
         __syncthreads();
         // pass 1: every source's records of this partition -> min rank per key
         for (int s = 0; s < pl.G; ++s) {
-            const u64 bucket = static_cast<u64>(s) * pl.np + part;
-            const unsigned cnt = min(B.in_cnt[bucket], static_cast<unsigned>(pl.cap));
-            const u64* recs = B.in + bucket * pl.cap * srec_words<W>();
+            const unsigned cnt = min(B.src_cnt[s][part], static_cast<unsigned>(pl.cap));
+            const u64* recs = B.src_recs[s] + part * pl.cap * srec_words<W>();
             for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
                 Set<W> key;
                 u64 rank;
@@ -273,9 +296,8 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
         if (!full) {
             // pass 2: the min-rank record of each key leaves its history
             for (int s = 0; s < pl.G; ++s) {
-                const u64 bucket = static_cast<u64>(s) * pl.np + part;
-                const unsigned cnt = min(B.in_cnt[bucket], static_cast<unsigned>(pl.cap));
-                const u64* recs = B.in + bucket * pl.cap * srec_words<W>();
+                const unsigned cnt = min(B.src_cnt[s][part], static_cast<unsigned>(pl.cap));
+                const u64* recs = B.src_recs[s] + part * pl.cap * srec_words<W>();
                 for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
                     Set<W> key;
                     u64 rank;
@@ -469,6 +491,7 @@ struct Shard {
     ShardCtl* h_ctl = nullptr;
     ShardBufs b{};
     u64 bloom_dirty = 0;  // words of the Bloom slice that may hold bits
+    int box_words = 0;    // W the boxes were sized for
 };
 
 class ShardSet {
@@ -545,10 +568,12 @@ public:
         t.d2h_bytes += d2h_;
         t.exchange_bytes += exchange_bytes_;
         t.reruns += reruns_;
+        t.offered += offered_;
+        t.unique += unique_;
     }
     void reset_counters() {
         decide_ms_ = layer_bytes_ = dedup_bytes_ = exchange_bytes_ = 0;
-        launches_ = expanded_ = h2d_ = d2h_ = reruns_ = 0;
+        launches_ = expanded_ = h2d_ = d2h_ = reruns_ = offered_ = unique_ = 0;
     }
 
     DecideResult decide(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg, int rounds,
@@ -577,6 +602,13 @@ public:
         while (r < rounds && !stopped) {
             const Plan pl = plan(r, count, prev, cfg, W);
             pl_round_parity_ = r & 1;
+            if (trace_)
+                std::fprintf(stderr, "[shard] k=%d r=%d E=%llu np=%llu cap=%llu recs/shard=%llu prev(exp=%llu routed=%llu uniq=%llu)\n",
+                             k, r, static_cast<unsigned long long>(std::accumulate(count.begin(), count.end(), u64{0})),
+                             static_cast<unsigned long long>(pl.np), static_cast<unsigned long long>(pl.cap),
+                             static_cast<unsigned long long>(G_ * pl.np * pl.cap),
+                             static_cast<unsigned long long>(prev.expanded), static_cast<unsigned long long>(prev.routed),
+                             static_cast<unsigned long long>(prev.unique));
             for (Shard& s : local_) prepare_round(s, pl, W, bloom, count);
             for (Shard& s : local_) launch_route(s, pl, W, cfg.use_mmw);
             exchange(pl, W);
@@ -615,6 +647,8 @@ public:
                 continue;
             }
             prev = c0.rs[r];
+            np_floor_ = 1;  // floors only widen the round that overflowed
+            cap_floor_ = 0;
             // every shard's kept count, shard-major (as k_shard_finish computed it)
             const u64 cap = host_round_cap(prev.expanded);
             u64 before = 0;
@@ -661,6 +695,8 @@ public:
             layer_bytes_ += wb * static_cast<double>(s.expanded + s.emitted);
             dedup_bytes_ += db * static_cast<double>(s.offered);
             expanded_ += s.expanded;
+            offered_ += s.offered;
+            unique_ += s.emitted;
             exchange_bytes_ += 8.0 * (W + 2) * static_cast<double>(s.routed) * (G_ - 1) / G_;
         }
         check(cudaEventRecord(ev_[1], stream_), "event");
@@ -692,9 +728,11 @@ private:
     u64 np_floor_ = 1, cap_floor_ = 0;
     u64 free_count_ = 0, max_states_ = 0;
     double decide_ms_ = 0, layer_bytes_ = 0, dedup_bytes_ = 0, exchange_bytes_ = 0;
-    uint64_t launches_ = 0, reruns_ = 0, expanded_ = 0, h2d_ = 0, d2h_ = 0;
+    uint64_t launches_ = 0, reruns_ = 0, expanded_ = 0, h2d_ = 0, d2h_ = 0, offered_ = 0, unique_ = 0;
     cudaEvent_t tev_[2] = {nullptr, nullptr};
-    int grid_route_ = 0, grid_owner_[2] = {0, 0};
+    int grid_route_[2] = {0, 0}, grid_owner_[2] = {0, 0};
+    bool tile_dedup_ = false;
+    bool trace_ = std::getenv("ETWG_SHARD_TRACE") != nullptr;
     u64* d_wit_ = nullptr;
     int pl_round_parity_ = 0;  // buffer holding the current round's input layer
 
@@ -720,7 +758,23 @@ private:
         allow(k_owner<1, true>, owner_smem_bytes<1>(), grid_owner_[0]);
         allow(k_owner<2, false>, owner_smem_bytes<2>(), grid_owner_[1]);
         allow(k_owner<2, true>, owner_smem_bytes<2>(), grid_owner_[1]);
-        grid_route_ = prop.multiProcessorCount * 4;
+        auto allow_route = [&](auto kernel, int bytes, int& grid) {
+            check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem");
+            int blocks = 0;
+            check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kRouteThreads, bytes), "occupancy");
+            grid = prop.multiProcessorCount * std::max(1, blocks);
+        };
+        // the no-dedup variants take the same grid (their occupancy is at least as high)
+        allow_route(k_route<1, false, true>, route_smem_bytes<1>(), grid_route_[0]);
+        allow_route(k_route<1, true, true>, route_smem_bytes<1>(), grid_route_[0]);
+        allow_route(k_route<2, false, true>, route_smem_bytes<2>(), grid_route_[1]);
+        allow_route(k_route<2, true, true>, route_smem_bytes<2>(), grid_route_[1]);
+        // ETWG_ROUTE_DEDUP=1 pre-dedups each tile of parents before routing.
+        // Off by default: a shard's layer is in (partition, rank) order, so
+        // consecutive parents are rarely siblings and the tile finds almost
+        // no duplicates (measured: 0.01 % of the routed records on G(48,0.2)).
+        const char* td = std::getenv("ETWG_ROUTE_DEDUP");
+        tile_dedup_ = td && td[0] == '1';
     }
 
     void create_shard(Shard& s, int me) {
@@ -869,20 +923,26 @@ private:
     void prepare_round(Shard& s, const Plan& pl, int W, bool bloom, const std::vector<u64>& count) {
         const u64 recs = static_cast<u64>(G_) * pl.np * pl.cap;
         const u64 cnts = static_cast<u64>(G_) * pl.np;
+        if (W != s.box_words) {  // record size changed: reallocate at the new width
+            s.b.box_cap = 0;
+            s.box_words = W;
+        }
         if (recs > s.b.box_cap || !s.b.out) {
-            const u64 cap = std::max<u64>(recs + recs / 4, u64{1} << 16);
+            const u64 cap = std::max<u64>(recs + recs / 16, u64{1} << 16);
             cudaFree(s.b.out);
             cudaFree(s.b.in);
-            check(cudaMalloc(&s.b.out, cap * 32), "outbox");
-            check(cudaMalloc(&s.b.in, cap * 32), "inbox");
+            s.b.in = nullptr;
+            check(cudaMalloc(&s.b.out, cap * 8 * (W + 2)), "outbox");
+            if (comm_) check(cudaMalloc(&s.b.in, cap * 8 * (W + 2)), "inbox");
             s.b.box_cap = cap;
         }
         if (cnts > s.b.cnt_cap || !s.b.out_cnt) {
             const u64 cap = std::max<u64>(cnts * 2, u64{1} << 12);
             cudaFree(s.b.out_cnt);
             cudaFree(s.b.in_cnt);
+            s.b.in_cnt = nullptr;
             check(cudaMalloc(&s.b.out_cnt, cap * 4), "outbox counts");
-            check(cudaMalloc(&s.b.in_cnt, cap * 4), "inbox counts");
+            if (comm_) check(cudaMalloc(&s.b.in_cnt, cap * 4), "inbox counts");
             s.b.cnt_cap = cap;
         }
         if (pl.np + 1 > s.b.tile_cap || !s.b.tiles) {
@@ -909,18 +969,26 @@ private:
             check(cudaMemsetAsync(s.b.bloom, 0, clear * 4, stream_), "bloom clear");
             s.bloom_dirty = words;
         }
-        (void)W;
+    }
+
+    template <int W, bool MMW>
+    void route_kernel(Shard& s, const Plan& p) {
+        if (tile_dedup_)
+            k_route<W, MMW, true><<<grid_route_[W - 1], kRouteThreads, route_smem_bytes<W>(), stream_>>>(
+                s.d_params, s.d_ctl, s.b, p);
+        else
+            k_route<W, MMW, false><<<grid_route_[W - 1], kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
     }
 
     void launch_route(Shard& s, const Plan& pl, int W, bool mmw) {
         Plan p = pl;
         p.me = s.me;
         if (W == 1) {
-            if (mmw) k_route<1, true><<<grid_route_, kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
-            else k_route<1, false><<<grid_route_, kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
+            if (mmw) route_kernel<1, true>(s, p);
+            else route_kernel<1, false>(s, p);
         } else {
-            if (mmw) k_route<2, true><<<grid_route_, kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
-            else k_route<2, false><<<grid_route_, kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
+            if (mmw) route_kernel<2, true>(s, p);
+            else route_kernel<2, false>(s, p);
         }
         check(cudaGetLastError(), "route launch");
         ++launches_;
@@ -929,6 +997,20 @@ private:
     void launch_owner(Shard& s, const Plan& pl, int W, bool bloom) {
         Plan p = pl;
         p.me = s.me;
+        const u64 block = pl.np * pl.cap * (W + 2);
+        for (int src = 0; src < G_; ++src) {
+            if (!comm_) {  // virtual shards: read the source's outbox in place
+                const Shard& from = local_[src];
+                s.b.src_recs[src] = from.b.out + s.me * block;
+                s.b.src_cnt[src] = from.b.out_cnt + s.me * pl.np;
+            } else if (src == s.me) {
+                s.b.src_recs[src] = s.b.out + s.me * block;
+                s.b.src_cnt[src] = s.b.out_cnt + s.me * pl.np;
+            } else {
+                s.b.src_recs[src] = s.b.in + src * block;
+                s.b.src_cnt[src] = s.b.in_cnt + src * pl.np;
+            }
+        }
         if (W == 1) {
             if (bloom) k_owner<1, true><<<grid_owner_[0], kOwnerThreads, owner_smem_bytes<1>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
             else k_owner<1, false><<<grid_owner_[0], kOwnerThreads, owner_smem_bytes<1>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
@@ -940,36 +1022,23 @@ private:
         ++launches_;
     }
 
-    // outbox block d of shard s -> inbox slot s of shard d
+    // outbox block d of shard s -> inbox slot s of shard d (NCCL); virtual
+    // shards and a shard's own block are read in place by k_owner
     void exchange(const Plan& pl, int W) {
-        const u64 rec_bytes = 8ull * (W + 2);
-        const u64 block = pl.np * pl.cap;
-        const u64 bytes = block * rec_bytes, cnt_bytes = pl.np * 4;
-        if (!comm_) {
-            for (Shard& src : local_)
-                for (Shard& dst : local_) {
-                    check(cudaMemcpyAsync(dst.b.in + src.me * block * (W + 2), src.b.out + dst.me * block * (W + 2),
-                                          bytes, cudaMemcpyDeviceToDevice, stream_), "exchange");
-                    check(cudaMemcpyAsync(dst.b.in_cnt + src.me * pl.np, src.b.out_cnt + dst.me * pl.np, cnt_bytes,
-                                          cudaMemcpyDeviceToDevice, stream_), "exchange counts");
-                }
-            return;
-        }
+        if (!comm_) return;
+        const u64 block = pl.np * pl.cap * (W + 2);
+        const u64 bytes = block * 8, cnt_bytes = pl.np * 4;
         Nccl& nc = Nccl::get();
         Shard& s = local_[0];
         nc.check(nc.GroupStart(), "group start");
         for (int d = 0; d < G_; ++d) {
             if (d == s.me) continue;
-            nc.check(nc.Send(s.b.out + d * block * (W + 2), bytes, ncclUint8, d, comm_, stream_), "send");
-            nc.check(nc.Recv(s.b.in + d * block * (W + 2), bytes, ncclUint8, d, comm_, stream_), "recv");
+            nc.check(nc.Send(s.b.out + d * block, bytes, ncclUint8, d, comm_, stream_), "send");
+            nc.check(nc.Recv(s.b.in + d * block, bytes, ncclUint8, d, comm_, stream_), "recv");
             nc.check(nc.Send(s.b.out_cnt + d * pl.np, cnt_bytes, ncclUint8, d, comm_, stream_), "send counts");
             nc.check(nc.Recv(s.b.in_cnt + d * pl.np, cnt_bytes, ncclUint8, d, comm_, stream_), "recv counts");
         }
         nc.check(nc.GroupEnd(), "group end");
-        check(cudaMemcpyAsync(s.b.in + s.me * block * (W + 2), s.b.out + s.me * block * (W + 2), bytes,
-                              cudaMemcpyDeviceToDevice, stream_), "self exchange");
-        check(cudaMemcpyAsync(s.b.in_cnt + s.me * pl.np, s.b.out_cnt + s.me * pl.np, cnt_bytes,
-                              cudaMemcpyDeviceToDevice, stream_), "self exchange counts");
     }
 
     void allgather_stats() {

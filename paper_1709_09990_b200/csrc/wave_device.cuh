@@ -194,8 +194,22 @@ __device__ __forceinline__ Set<W> param_set(const u64 (&w)[2]) {
 // K1: candidate evaluation (replaces expand_range + q_set, dp.cpp:39-69,
 // graph.hpp:61-78, and the MMW prune driven at dp.cpp:51-63)
 
-// For every u in S: R[u] = N(K_u) \ S, the outside boundary of u's component
-// K_u of G[S] (flood fill over bitmask rows, one pass per component).
+// Rank of u among the members of S (u in S): R is indexed by it, so a
+// layer's states (all of size |S| = round+1) touch only the first |S|
+// entries and the warp's slice of local memory stays L1-resident.
+template <int W>
+__device__ __forceinline__ int member_rank(const Set<W>& S, int u) {
+    if constexpr (W == 1) {
+        return __popcll(S.w[0] & ((u64{1} << u) - 1));
+    } else {
+        return u < 64 ? __popcll(S.w[0] & ((u64{1} << u) - 1))
+                      : __popcll(S.w[0]) + __popcll(S.w[1] & ((u64{1} << (u - 64)) - 1));
+    }
+}
+
+// For every u in S: R[rank(u)] = N(K_u) \ S, the outside boundary of u's
+// component K_u of G[S] (flood fill over bitmask rows, one pass per
+// component).
 template <int W>
 __device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>& S, Set<W>* R) {
     Set<W> rem = S;
@@ -212,7 +226,7 @@ __device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>&
         }
         rem = rem - comp;
         const Set<W> boundary = nb - S;
-        for (int u : members(comp)) R[u] = boundary;
+        for (int u : members(comp)) R[member_rank<W>(S, u)] = boundary;
     }
 }
 
@@ -223,7 +237,7 @@ template <int W>
 __device__ __forceinline__ Set<W> reach_from(const Set<W>* adj, const Set<W>& S, const Set<W>* R,
                                              int v) {
     Set<W> q = adj[v] - S;
-    for (int u : members(adj[v] & S)) q |= R[u];
+    for (int u : members(adj[v] & S)) q |= R[member_rank<W>(S, u)];
     q.del(v);
     return q;
 }

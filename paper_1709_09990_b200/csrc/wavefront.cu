@@ -209,6 +209,11 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
         Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
+        if ((P->flags & 32) && valid) {  // timing A/B only: K1 evaluated twice
+            u64 dummy = 0;
+            const Set<W> M2 = candidates<W, MMW>(adj, P->n, P->k, S, forbidden, dummy);
+            if (M2 != M) M = M2;
+        }
         offered += M.count();
         if (P->flags & 16) tile_dedup<W, tile_slots<W>()>(ts, win, S, M);  // flag 16: A/B only
         winners += M.count();
@@ -1180,12 +1185,29 @@ private:
 
     // SURVEY §8d algorithmic bytes: W*E_in + W*E_out + D*P per round
     void account(const std::vector<LayerStats>& rounds, int W, const DpConfig& cfg) {
-        const double wb = 8.0 * W + 4.0;
-        const double db = cfg.dedup == DedupMode::bloom ? 4.0 * cfg.bloom_hashes : (W == 1 ? 16.0 : 24.0);
+        const double wb = 8.0 * W + 4.0, sb = 8.0 * W;
+        const bool bloom = cfg.dedup == DedupMode::bloom;
+        const double db = bloom ? 4.0 * cfg.bloom_hashes : (W == 1 ? 16.0 : 24.0);
         for (const LayerStats& s : rounds) {
-            prof.t.layer_bytes += wb * static_cast<double>(s.expanded + s.emitted);
-            prof.t.dedup_bytes += db * static_cast<double>(s.emitted + s.duplicates);
+            const double E = static_cast<double>(s.expanded), U = static_cast<double>(s.emitted);
+            const double P = static_cast<double>(s.emitted + s.duplicates);
+            prof.t.layer_bytes += wb * (E + U);
+            prof.t.dedup_bytes += db * P;
             prof.t.expanded += s.expanded;
+            prof.t.offered += s.emitted + s.duplicates;
+            prof.t.unique += s.emitted;
+            if (bloom) {
+                // k_bloom_dedup: parent read + novel-mask write + h probe words per child
+                prof.t.insert_bytes += 2 * sb * E + db * P;
+            } else {
+                // k_exact_scatter: parent read, winner-mask clear, one record per child;
+                // k_exact_part: record read, one winner-mask OR per distinct key
+                const double rec = 8.0 * W + 8.0;
+                prof.t.expand_bytes += 2 * sb * E + rec * P;
+                prof.t.insert_bytes += rec * P + 8.0 * U;
+            }
+            // k_append: parent + history + mask read, state + history written
+            prof.t.append_bytes += (sb + 4.0 + sb) * E + wb * U;
         }
     }
 };

@@ -159,3 +159,18 @@ def test_sharded_solve_stats_identical(E, shards):
     res = E.solve(g, E.Options(dedup="exact", emit_order=True))
     width, valid = g.check_order(res.order)
     assert res.value == 22 and valid and width <= 22
+
+
+def test_sharded_layers_live_on_their_owner(E, shards):
+    """The observer concatenates the shards' slices in shard order, so the
+    owner (tests/shard_model.py's restatement of shard.cu owner_of) of
+    consecutive states never decreases: every state sits on its owner."""
+    from shard_model import owner_of
+    rows = G.random_graph(1, 40, 0.3)
+    shards(3)
+    run = E.decide(rows, 21, dedup="exact")
+    for r, layer in enumerate(run.layers):
+        owners = [owner_of(s, 3) for s, _ in layer]
+        assert owners == sorted(owners), r
+        if len(layer) > 100:
+            assert set(owners) == {0, 1, 2}, r

@@ -7,6 +7,8 @@ from paper_1709_09990_b200 import elimtw as E, generators as G
 k = int(sys.argv[1]); dedup = sys.argv[2]; reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 n = int(os.environ.get("PROBE_N", "48")); p = float(os.environ.get("PROBE_P", "0.2"))
 rows = G.random_graph(1, n, p)
+if int(os.environ.get("VSHARDS", "1")) > 1:
+    E.set_virtual_shards(int(os.environ["VSHARDS"]))
 for _ in range(reps):
     t0 = time.perf_counter()
     r = E.decide(rows, k, dedup=dedup, cap=1 << 31, keep_layers=False)
