@@ -60,11 +60,18 @@ template <int W>
 constexpr int owner_slots() { return 2048; }
 template <int W>
 constexpr int owner_target() { return 640; }  // distinct keys aimed for per partition
+// Child record: {key words, parent index << 32 | history}. The emission
+// rank (source shard, parent index, vertex) is rebuilt by the owner: the
+// source is the block it reads, the vertex the history's low byte.
 template <int W>
-constexpr int srec_words() { return W + 2; }  // {key words, rank, history}
+constexpr int srec_words() { return W + 1; }
 template <int W>
 constexpr int owner_smem_bytes() {
-    return owner_slots<W>() * (8 * W + 8 + 4 + 8);  // keys, ranks, histories, sort keys
+    return owner_slots<W>() * (8 * W + 16 + 8);  // keys, {min rank, history}, sort keys
+}
+
+__device__ __forceinline__ u64 owner_rank(int src, u64 packed) {
+    return (static_cast<u64>(src) << 40) | ((packed >> 32) << 7) | (packed & 0x7F);
 }
 
 enum ShardAbort : unsigned { kAbortLayer = 1, kAbortRecs = 2, kAbortParts = 4 };
@@ -161,7 +168,6 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
     const Set<W> forbidden = param_set<W>(P->forbidden);
     const u64* in = B.keys[r & 1];
     const unsigned* hin = B.hist[r & 1];
-    const u64 src_tag = static_cast<u64>(pl.me) << 40;
     const u64 ntiles = (E + kRouteThreads - 1) / kRouteThreads;
     u64 offered = 0, pruned = 0, routed = 0;
     bool full = false;
@@ -197,10 +203,14 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
                 const unsigned slot = atomicAdd(B.out_cnt + bucket, 1u);
                 if (slot < pl.cap) {
                     u64* rec = B.out + (bucket * pl.cap + slot) * srec_words<W>();
-#pragma unroll
-                    for (int w = 0; w < W; ++w) rec[w] = key.w[w];
-                    rec[W] = src_tag | child_rank<W>(warp_base + src, v);
-                    rec[W + 1] = (static_cast<u64>(Hs) << 8) | static_cast<u64>(v & 0xFF);  // push_history
+                    const u64 packed = ((warp_base + src) << 32) | ((Hs << 8) | static_cast<unsigned>(v));  // push_history
+                    if constexpr (W == 1) {
+                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], packed);
+                    } else {
+                        rec[0] = key.w[0];
+                        rec[1] = key.w[1];
+                        rec[2] = packed;
+                    }
                 } else {
                     full = true;
                 }
@@ -230,16 +240,38 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
 // k_owner: per partition exact dedup (+ Bloom), rank sort, ordered append
 
 template <int W>
-__device__ __forceinline__ void load_srec(const u64* rec, Set<W>& key, u64& rank, unsigned& hist) {
+__device__ __forceinline__ void load_srec(const u64* rec, Set<W>& key, u64& packed) {
     if constexpr (W == 1) {
-        key.w[0] = __ldcs(rec);
+        const ulonglong2 r = __ldcs(reinterpret_cast<const ulonglong2*>(rec));
+        key.w[0] = r.x;
+        packed = r.y;
     } else {
-        const ulonglong2 k2 = __ldcs(reinterpret_cast<const ulonglong2*>(rec));
-        key.w[0] = k2.x;
-        key.w[1] = k2.y;
+        key.w[0] = __ldcs(rec);
+        key.w[1] = __ldcs(rec + 1);
+        packed = __ldcs(rec + 2);
     }
-    rank = __ldcs(rec + W);
-    hist = static_cast<unsigned>(__ldcs(rec + W + 1));
+}
+
+// {rank, history} of a table slot lowered to (rank, hist) if rank is smaller
+// (128-bit CAS in shared memory, so the history always belongs to the rank)
+__device__ __forceinline__ void smem_min_pair(ulonglong2* slot, u64 rank, u64 hist) {
+    u64 er = slot->x, eh = slot->y;
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(slot));
+    while (rank < er) {
+        u64 orr, oh;
+        asm volatile(
+            "{\n\t.reg .b128 c, s, d;\n\t"
+            "mov.b128 c, {%2, %3};\n\t"
+            "mov.b128 s, {%4, %5};\n\t"
+            "atom.shared.cas.b128 d, [%6], c, s;\n\t"
+            "mov.b128 {%0, %1}, d;\n\t}"
+            : "=l"(orr), "=l"(oh)
+            : "l"(er), "l"(eh), "l"(rank), "l"(hist), "r"(sa)
+            : "memory");
+        if (orr == er && oh == eh) return;
+        er = orr;
+        eh = oh;
+    }
 }
 
 template <int W, bool BLOOM>
@@ -247,10 +279,9 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
                                                          ShardBufs B, Plan pl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int SLOTS = owner_slots<W>();
-    u64* keys = reinterpret_cast<u64*>(smem_raw);
-    u64* ranks = keys + SLOTS * W;
-    u64* sortk = ranks + SLOTS;
-    unsigned* hists = reinterpret_cast<unsigned*>(sortk + SLOTS);
+    ulonglong2* vals = reinterpret_cast<ulonglong2*>(smem_raw);  // {min rank, history}
+    u64* keys = reinterpret_cast<u64*>(vals + SLOTS);
+    u64* sortk = keys + SLOTS * W;
     __shared__ unsigned s_full, s_cnt;
     __shared__ u64 s_part, s_prefix;
     if (C->stop) return;
@@ -264,21 +295,21 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
         const u64 part = s_part;
         if (part >= pl.np) break;
         for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) keys[i] = 0;
-        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) ranks[i] = ~u64{0};
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) vals[i] = make_ulonglong2(~u64{0}, 0);
         if (threadIdx.x == 0) {
             s_full = 0;
             s_cnt = 0;
         }
         __syncthreads();
-        // pass 1: every source's records of this partition -> min rank per key
+        // every source's records of this partition -> min emission rank per
+        // key, with that emission's history (dp.cpp:140-151)
         for (int s = 0; s < pl.G; ++s) {
             const unsigned cnt = min(B.src_cnt[s][part], static_cast<unsigned>(pl.cap));
             const u64* recs = B.src_recs[s] + part * pl.cap * srec_words<W>();
             for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
                 Set<W> key;
-                u64 rank;
-                unsigned hist;
-                load_srec<W>(recs + static_cast<u64>(i) * srec_words<W>(), key, rank, hist);
+                u64 packed;
+                load_srec<W>(recs + static_cast<u64>(i) * srec_words<W>(), key, packed);
                 unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
                 bool placed = false;
                 for (int probe = 0; probe < SLOTS && !placed; ++probe) {
@@ -286,7 +317,7 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
                     if (!placed) h = (h + 1) & (SLOTS - 1);
                 }
                 if (placed)
-                    atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), rank);
+                    smem_min_pair(vals + h, owner_rank(s, packed), packed & 0xFFFFFFFFull);
                 else
                     s_full = 1;
             }
@@ -294,24 +325,10 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
         __syncthreads();
         const bool full = s_full != 0;
         if (!full) {
-            // pass 2: the min-rank record of each key leaves its history
-            for (int s = 0; s < pl.G; ++s) {
-                const unsigned cnt = min(B.src_cnt[s][part], static_cast<unsigned>(pl.cap));
-                const u64* recs = B.src_recs[s] + part * pl.cap * srec_words<W>();
-                for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
-                    Set<W> key;
-                    u64 rank;
-                    unsigned hist;
-                    load_srec<W>(recs + static_cast<u64>(i) * srec_words<W>(), key, rank, hist);
-                    const int slot = smem_find<W>(keys, static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1),
-                                                  SLOTS - 1, key, SLOTS);
-                    if (slot >= 0 && ranks[slot] == rank) hists[slot] = hist;
-                }
-            }
-            __syncthreads();
             // compact the distinct keys (Bloom mode: only those the filter calls novel)
             for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
-                if (ranks[i] == ~u64{0}) continue;
+                const u64 rank = vals[i].x;
+                if (rank == ~u64{0}) continue;
                 bool keep = true;
                 if constexpr (BLOOM) {
                     Set<W> key;
@@ -331,7 +348,7 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
                         if (pos >= pl.bloom_m) pos -= pl.bloom_m;
                     }
                 }
-                if (keep) sortk[atomicAdd(&s_cnt, 1u)] = (ranks[i] << 12) | static_cast<u64>(i);
+                if (keep) sortk[atomicAdd(&s_cnt, 1u)] = (rank << 12) | static_cast<u64>(i);
             }
         }
         __syncthreads();
@@ -369,7 +386,7 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
 #pragma unroll
             for (int w = 0; w < W; ++w) key.w[w] = keys[W * slot + w];
             store_set<W>(out, pos, key);
-            hout[pos] = hists[slot];
+            hout[pos] = static_cast<unsigned>(vals[slot].y);
         }
         if (threadIdx.x == 0) {
             if (full) {
@@ -502,7 +519,9 @@ public:
     }
     std::mutex mu;
 
-    bool active() const { return G_ > 1; }
+    // a one-rank NCCL communicator is active too: it runs the whole NCCL
+    // host flow (allgather, witness broadcast) on a single GPU
+    bool active() const { return G_ > 1 || comm_ != nullptr; }
 
     void set_virtual(int G) {
         if (G < 1 || G > kMaxShards) throw std::invalid_argument("virtual shard count must be 1..8");
@@ -609,6 +628,8 @@ public:
                              static_cast<unsigned long long>(G_ * pl.np * pl.cap),
                              static_cast<unsigned long long>(prev.expanded), static_cast<unsigned long long>(prev.routed),
                              static_cast<unsigned long long>(prev.unique));
+            for (u64 c : count)
+                if (c >> 32) throw DeviceError("sharded layer slice exceeds 2^32 states");
             for (Shard& s : local_) prepare_round(s, pl, W, bloom, count);
             for (Shard& s : local_) launch_route(s, pl, W, cfg.use_mmw);
             exchange(pl, W);
@@ -697,7 +718,7 @@ public:
             expanded_ += s.expanded;
             offered_ += s.offered;
             unique_ += s.emitted;
-            exchange_bytes_ += 8.0 * (W + 2) * static_cast<double>(s.routed) * (G_ - 1) / G_;
+            exchange_bytes_ += 8.0 * (W + 1) * static_cast<double>(s.routed) * (G_ - 1) / G_;
         }
         check(cudaEventRecord(ev_[1], stream_), "event");
         check(cudaEventSynchronize(ev_[1]), "event sync");
@@ -932,8 +953,8 @@ private:
             cudaFree(s.b.out);
             cudaFree(s.b.in);
             s.b.in = nullptr;
-            check(cudaMalloc(&s.b.out, cap * 8 * (W + 2)), "outbox");
-            if (comm_) check(cudaMalloc(&s.b.in, cap * 8 * (W + 2)), "inbox");
+            check(cudaMalloc(&s.b.out, cap * 8 * (W + 1)), "outbox");
+            if (comm_) check(cudaMalloc(&s.b.in, cap * 8 * (W + 1)), "inbox");
             s.b.box_cap = cap;
         }
         if (cnts > s.b.cnt_cap || !s.b.out_cnt) {
@@ -997,7 +1018,7 @@ private:
     void launch_owner(Shard& s, const Plan& pl, int W, bool bloom) {
         Plan p = pl;
         p.me = s.me;
-        const u64 block = pl.np * pl.cap * (W + 2);
+        const u64 block = pl.np * pl.cap * (W + 1);
         for (int src = 0; src < G_; ++src) {
             if (!comm_) {  // virtual shards: read the source's outbox in place
                 const Shard& from = local_[src];
@@ -1026,7 +1047,7 @@ private:
     // shards and a shard's own block are read in place by k_owner
     void exchange(const Plan& pl, int W) {
         if (!comm_) return;
-        const u64 block = pl.np * pl.cap * (W + 2);
+        const u64 block = pl.np * pl.cap * (W + 1);
         const u64 bytes = block * 8, cnt_bytes = pl.np * 4;
         Nccl& nc = Nccl::get();
         Shard& s = local_[0];

@@ -174,3 +174,24 @@ def test_sharded_layers_live_on_their_owner(E, shards):
         assert owners == sorted(owners), r
         if len(layer) > 100:
             assert set(owners) == {0, 1, 2}, r
+
+
+def test_nccl_one_rank_communicator(E, gpu):
+    """The NCCL host flow (ncclAllGather of the round counters, the witness
+    ncclBroadcast, inbox pointer tables) on a one-rank communicator: results
+    equal the single-device engine's."""
+    rows = G.random_graph(1, 40, 0.3)
+    want = {k: E.decide(rows, k, dedup="exact") for k in (21, 22)}
+    E.shard_init(E.nccl_unique_id(), 0, 1, gpu["device"])
+    try:
+        assert E.shard_info() == {"world": 1, "rank": 0, "virtual": False}
+        for k, w in want.items():
+            got = E.decide(rows, k, dedup="exact")
+            assert got.outcome == w.outcome
+            assert _counters(got) == _counters(w)
+            assert _sets(got) == _sets(w)
+            _check_witness(rows, k, got)
+        res = E.solve(E.Graph.from_rows(rows), E.Options(dedup="exact"))
+        assert res.value == 22
+    finally:
+        E.shard_release()

@@ -1,13 +1,6 @@
 mkdir -p gpurun_out
-cat > /tmp/ab.py <<'PY'
-import os, sys, time
-sys.path.insert(0, os.getcwd())
-from paper_1709_09990_b200 import elimtw as E, generators as G
-rows = G.random_graph(1, 48, 0.2)
-E.decide(rows, 22, dedup="exact", cap=1 << 31, keep_layers=False)
-E.set_profiling(True); E.reset_times()
-E.decide(rows, 22, dedup="exact", cap=1 << 31, keep_layers=False)
-t = E.times(); print({k: round(t[k], 1) for k in ("expand_ms", "insert_ms", "append_ms")})
-PY
-python /tmp/ab.py
-ETWG_DEBUG=32 python /tmp/ab.py
+timeout 900 python -m pytest tests/test_gpu_shard.py -x -q --timeout 300 2>&1 | grep -E "passed|failed|Error|assert" | head
+timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | head -2
+VSHARDS=2 timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | head -2
+VSHARDS=8 timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | head -2
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_vs2b.csv env VSHARDS=2 python tools/prof_decide.py 22 exact 1 > /dev/null 2>&1
