@@ -194,22 +194,9 @@ __device__ __forceinline__ Set<W> param_set(const u64 (&w)[2]) {
 // K1: candidate evaluation (replaces expand_range + q_set, dp.cpp:39-69,
 // graph.hpp:61-78, and the MMW prune driven at dp.cpp:51-63)
 
-// Rank of u among the members of S (u in S): R is indexed by it, so a
-// layer's states (all of size |S| = round+1) touch only the first |S|
-// entries and the warp's slice of local memory stays L1-resident.
-template <int W>
-__device__ __forceinline__ int member_rank(const Set<W>& S, int u) {
-    if constexpr (W == 1) {
-        return __popcll(S.w[0] & ((u64{1} << u) - 1));
-    } else {
-        return u < 64 ? __popcll(S.w[0] & ((u64{1} << u) - 1))
-                      : __popcll(S.w[0]) + __popcll(S.w[1] & ((u64{1} << (u - 64)) - 1));
-    }
-}
-
-// For every u in S: R[rank(u)] = N(K_u) \ S, the outside boundary of u's
+// For every u in S: R[u] = N(K_u) \ S, the outside boundary of u's
 // component K_u of G[S] (flood fill over bitmask rows, one pass per
-// component).
+// component). Components without outside neighbours touch no candidate.
 template <int W>
 __device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>& S, Set<W>* R) {
     Set<W> rem = S;
@@ -226,7 +213,8 @@ __device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>&
         }
         rem = rem - comp;
         const Set<W> boundary = nb - S;
-        for (int u : members(comp)) R[member_rank<W>(S, u)] = boundary;
+        if (boundary.none()) continue;
+        for (int u : members(comp)) R[u] = boundary;
     }
 }
 
@@ -237,7 +225,7 @@ template <int W>
 __device__ __forceinline__ Set<W> reach_from(const Set<W>* adj, const Set<W>& S, const Set<W>* R,
                                              int v) {
     Set<W> q = adj[v] - S;
-    for (int u : members(adj[v] & S)) q |= R[member_rank<W>(S, u)];
+    for (int u : members(adj[v] & S)) q |= R[u];
     q.del(v);
     return q;
 }
@@ -283,8 +271,10 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
     Set<W> R[N];
     component_reach<W>(adj, S, R);
     if constexpr (!MMW) {
-        for (int v : members(eligible))
+        for (int v : members(eligible)) {
+            if ((adj[v] - S).count() > k) continue;  // |Q(S,v)| >= |N(v) \ S|
             if (reach_from<W>(adj, S, R, v).count() <= k) keep.add(v);
+        }
     } else {
         Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
         for (int w : members(open)) rows[w] = reach_from<W>(adj, S, R, w);

@@ -1,10 +1,4 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q --timeout 600 2>&1 | tail -2
-timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; tail -2 gpurun_out/bench_full.err
-python tools/prof_decide.py 22 exact 1 > gpurun_out/decide22_stats.txt 2>&1
-python tools/ncu_top.py k_exact_scatter ncu_scatter -- python tools/prof_decide.py 22 exact 1
-python tools/ncu_top.py k_exact_part ncu_part -- python tools/prof_decide.py 22 exact 1
-python tools/ncu_top.py k_append ncu_append -- python tools/prof_decide.py 22 exact 1
-python tools/ncu_top.py k_route ncu_route -- env VSHARDS=2 python tools/prof_decide.py 22 exact 1
-python tools/ncu_top.py k_owner ncu_owner -- env VSHARDS=2 python tools/prof_decide.py 22 exact 1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_g48_solve.csv python tools/prof_g48.py exact > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q --timeout 600 2>&1 | tail -2
+timeout 300 python tools/prof_decide.py 22 exact 3 2>&1 | head -3
+timeout 600 python bench.py --no-extras 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['value'], d['ms_per_step'], d['roofline']['kernel_ms'])"
