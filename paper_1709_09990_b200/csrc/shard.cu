@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
         const unsigned H = valid ? hin[idx] : 0u;
-        Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
+        Set<W> M = valid ? candidates<W, MMW, true>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
         offered += M.count();
         if constexpr (TILE) {
             tile_set_clear<W, route_tile_slots<W>()>(ts);
@@ -785,17 +785,31 @@ private:
             check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kRouteThreads, bytes), "occupancy");
             grid = prop.multiProcessorCount * std::max(1, blocks);
         };
-        // the no-dedup variants take the same grid (their occupancy is at least as high)
-        allow_route(k_route<1, false, true>, route_smem_bytes<1>(), grid_route_[0]);
-        allow_route(k_route<1, true, true>, route_smem_bytes<1>(), grid_route_[0]);
-        allow_route(k_route<2, false, true>, route_smem_bytes<2>(), grid_route_[1]);
-        allow_route(k_route<2, true, true>, route_smem_bytes<2>(), grid_route_[1]);
         // ETWG_ROUTE_DEDUP=1 pre-dedups each tile of parents before routing.
         // Off by default: a shard's layer is in (partition, rank) order, so
         // consecutive parents are rarely siblings and the tile finds almost
         // no duplicates (measured: 0.01 % of the routed records on G(48,0.2)).
         const char* td = std::getenv("ETWG_ROUTE_DEDUP");
         tile_dedup_ = td && td[0] == '1';
+        // grid = resident CTAs of the variant that will run (the MMW one bounds it)
+        int g_mmw[2];
+        if (tile_dedup_) {
+            allow_route(k_route<1, false, true>, route_smem_bytes<1>(), grid_route_[0]);
+            allow_route(k_route<1, true, true>, route_smem_bytes<1>(), g_mmw[0]);
+            allow_route(k_route<2, false, true>, route_smem_bytes<2>(), grid_route_[1]);
+            allow_route(k_route<2, true, true>, route_smem_bytes<2>(), g_mmw[1]);
+        } else {
+            allow_route(k_route<1, false, false>, 0, grid_route_[0]);
+            allow_route(k_route<1, true, false>, 0, g_mmw[0]);
+            allow_route(k_route<2, false, false>, 0, grid_route_[1]);
+            allow_route(k_route<2, true, false>, 0, g_mmw[1]);
+        }
+        grid_route_[0] = std::min(grid_route_[0], g_mmw[0]);
+        grid_route_[1] = std::min(grid_route_[1], g_mmw[1]);
+        if (const char* c = std::getenv("ETWG_ROUTE_CTAS")) {  // CTAs per SM (tuning sweeps)
+            const int per = std::atoi(c);
+            for (int w = 0; w < 2; ++w) grid_route_[w] = std::min(grid_route_[w], prop.multiProcessorCount * per);
+        }
     }
 
     void create_shard(Shard& s, int me) {

@@ -194,10 +194,29 @@ __device__ __forceinline__ Set<W> param_set(const u64 (&w)[2]) {
 // K1: candidate evaluation (replaces expand_range + q_set, dp.cpp:39-69,
 // graph.hpp:61-78, and the MMW prune driven at dp.cpp:51-63)
 
-// For every u in S: R[u] = N(K_u) \ S, the outside boundary of u's
+// Slot of member u of S in the per-parent boundary table R. Vertex-indexed
+// (COMPACT = false) costs nothing; rank-indexed (COMPACT = true, the rank of
+// u among S's members) keeps a warp's touched slots within the first |S|
+// entries when the warp's parents are unrelated (a sharded layer is in hash
+// order), so its slice of local memory stays L1-resident. Measured: vertex
+// indexing is faster on rank-ordered layers (single device), rank indexing
+// on hash-ordered ones (shards).
+template <int W, bool COMPACT>
+__device__ __forceinline__ int reach_slot(const Set<W>& S, int u) {
+    if constexpr (!COMPACT) {
+        return u;
+    } else if constexpr (W == 1) {
+        return __popcll(S.w[0] & ((u64{1} << u) - 1));
+    } else {
+        return u < 64 ? __popcll(S.w[0] & ((u64{1} << u) - 1))
+                      : __popcll(S.w[0]) + __popcll(S.w[1] & ((u64{1} << (u - 64)) - 1));
+    }
+}
+
+// For every u in S: R[slot(u)] = N(K_u) \ S, the outside boundary of u's
 // component K_u of G[S] (flood fill over bitmask rows, one pass per
 // component). Components without outside neighbours touch no candidate.
-template <int W>
+template <int W, bool COMPACT>
 __device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>& S, Set<W>* R) {
     Set<W> rem = S;
     while (rem.any()) {
@@ -214,18 +233,18 @@ __device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>&
         rem = rem - comp;
         const Set<W> boundary = nb - S;
         if (boundary.none()) continue;
-        for (int u : members(comp)) R[u] = boundary;
+        for (int u : members(comp)) R[reach_slot<W, COMPACT>(S, u)] = boundary;
     }
 }
 
 // Q(S,v) (graph.hpp:61-78): v's own outside neighbours plus the boundary of
 // every component of G[S] that v touches, i.e. of K_u for u in N(v) & S.
 // Costs |N(v) & S| mask ORs instead of a DFS per (S, v).
-template <int W>
+template <int W, bool COMPACT>
 __device__ __forceinline__ Set<W> reach_from(const Set<W>* adj, const Set<W>& S, const Set<W>* R,
                                              int v) {
     Set<W> q = adj[v] - S;
-    for (int u : members(adj[v] & S)) q |= R[u];
+    for (int u : members(adj[v] & S)) q |= R[reach_slot<W, COMPACT>(S, u)];
     q.del(v);
     return q;
 }
@@ -260,7 +279,7 @@ __device__ int mmw_child(const Set<W>* adj, int n, int cap, const Set<W>& S, int
     return minor_min_width<W>(m, cap);
 }
 
-template <int W, bool MMW>
+template <int W, bool MMW, bool COMPACT = false>
 __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, const Set<W>& S,
                                              const Set<W>& forbidden, u64& pruned) {
     constexpr int N = 64 * W;
@@ -269,15 +288,15 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
     Set<W> keep = Set<W>::zero();
     if (eligible.none()) return keep;
     Set<W> R[N];
-    component_reach<W>(adj, S, R);
+    component_reach<W, COMPACT>(adj, S, R);
     if constexpr (!MMW) {
         for (int v : members(eligible)) {
             if ((adj[v] - S).count() > k) continue;  // |Q(S,v)| >= |N(v) \ S|
-            if (reach_from<W>(adj, S, R, v).count() <= k) keep.add(v);
+            if (reach_from<W, COMPACT>(adj, S, R, v).count() <= k) keep.add(v);
         }
     } else {
         Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
-        for (int w : members(open)) rows[w] = reach_from<W>(adj, S, R, w);
+        for (int w : members(open)) rows[w] = reach_from<W, COMPACT>(adj, S, R, w);
         for (int v : members(eligible)) {
             if (rows[v].count() > k) continue;
             if (mmw_child<W>(adj, n, k, S, v, rows) > k) {

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
     const u64 ntiles = (E + kThreads - 1) / kThreads;
     u64 offered = 0, pruned = 0, winners = 0;
     for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        tile_set_clear<W, tile_slots<W>()>(ts);
+        if (P->flags & 16) tile_set_clear<W, tile_slots<W>()>(ts);  // launch carries the tile set
         if (threadIdx.x == 0) s_stop = *reinterpret_cast<volatile unsigned*>(&C->abort);
         __syncthreads();
         if (s_stop) break;
@@ -774,6 +774,7 @@ private:
     int grid_fused_ = 0;
     int grid_exact_[2] = {0, 0};
     int grid_part_[2] = {0, 0};
+    int tile_smem_ = 0;  // 1: scatter launches carry the tile set (ETWG_DEBUG=16)
 
     // Epochs tag look-back statuses (24 bits); on wrap-around the status
     // array is cleared so a status from 2^24 attempts ago cannot match.
@@ -833,10 +834,23 @@ private:
             check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, bytes), "occupancy");
             grid = prop.multiProcessorCount * std::max(1, blocks);
         };
-        allow_exact(k_exact_scatter<1, false>, tile_set_bytes<1>(), grid_exact_[0]);
-        allow_exact(k_exact_scatter<1, true>, tile_set_bytes<1>(), grid_exact_[0]);
-        allow_exact(k_exact_scatter<2, false>, tile_set_bytes<2>(), grid_exact_[1]);
-        allow_exact(k_exact_scatter<2, true>, tile_set_bytes<2>(), grid_exact_[1]);
+        // the tile set is only used by the ETWG_DEBUG=16 A/B; the default launch
+        // takes no dynamic shared memory and the occupancy that allows
+        tile_smem_ = 0;
+        if (const char* dbg = std::getenv("ETWG_DEBUG"))
+            if (std::atoi(dbg) & 16) tile_smem_ = 1;
+        allow_exact(k_exact_scatter<1, false>, tile_smem_ ? tile_set_bytes<1>() : 0, grid_exact_[0]);
+        allow_exact(k_exact_scatter<2, false>, tile_smem_ ? tile_set_bytes<2>() : 0, grid_exact_[1]);
+        int g_mmw[2];
+        allow_exact(k_exact_scatter<1, true>, tile_smem_ ? tile_set_bytes<1>() : 0, g_mmw[0]);
+        allow_exact(k_exact_scatter<2, true>, tile_smem_ ? tile_set_bytes<2>() : 0, g_mmw[1]);
+        grid_exact_[0] = std::min(grid_exact_[0], g_mmw[0]);
+        grid_exact_[1] = std::min(grid_exact_[1], g_mmw[1]);
+        if (const char* c = std::getenv("ETWG_SCATTER_CTAS")) {  // CTAs per SM (tuning sweeps)
+            const int per = std::atoi(c);
+            for (int w = 0; w < 2; ++w) grid_exact_[w] = std::min(grid_exact_[w], prop.multiProcessorCount * per);
+        }
+        if (tile_smem_) tile_smem_ = 1;
         auto allow_part = [&](auto kernel, int bytes, int& grid) {
             check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                   "smem attribute");
@@ -1032,10 +1046,10 @@ private:
             return;
         }
         if (cfg.use_mmw)
-            timed_launch([&] { k_exact_scatter<W, true><<<grid_exact_[W - 1], kThreads, tile_set_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_exact_scatter<W, true><<<grid_exact_[W - 1], kThreads, tile_smem_ ? tile_set_bytes<W>() : 0, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
         else
-            timed_launch([&] { k_exact_scatter<W, false><<<grid_exact_[W - 1], kThreads, tile_set_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_exact_scatter<W, false><<<grid_exact_[W - 1], kThreads, tile_smem_ ? tile_set_bytes<W>() : 0, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
         timed_launch([&] { k_exact_part<W><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_ctl_, b_); },
                      prof.t.insert_ms, prof.t.insert_launches);

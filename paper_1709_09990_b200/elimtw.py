@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libelimtw.so")
+LIB_PATH = os.environ.get("ETWG_LIB") or os.path.join(_HERE, "libelimtw.so")
 
 ETW_OK, ETW_ERROR_PARSE, ETW_ERROR_INVALID_ARGUMENT, ETW_ERROR_INTERNAL = 0, 1, 2, 3
 FORMATS = {"auto": 0, "gr": 1, "dimacs": 2}
