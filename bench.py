@@ -22,8 +22,8 @@ Unit of work = LayerStats::expanded (dp.cpp:77), summed over the solve:
             cores, rank 0 at N=1: a bounded sample of the same sweep — the
             reference's decide on the first attempts (k = 11, 12, ...) of the
             same block with the same improved graphs and forbidden clique
-  bloom     Bloom-mode false-positive probe and a Bloom-vs-exact timing on
-            G(40,0.3) (BASELINE cfg 3), N=1 only
+  bloom     Bloom-mode false-positive probe, the bench graph in Bloom mode,
+            and a Bloom-vs-exact timing on G(40,0.3) (BASELINE cfg 3), N=1 only
 
 N > 1 (torchrun): every rank becomes one owner shard (paper_1709_09990_b200/
 distributed.py; states routed to hash owners over NCCL each round) and all
@@ -292,6 +292,17 @@ def bloom_probe(E, G):
                            "exact_novel": u, "bloom_novel": b, "false_positives": u - b,
                            "measured_fp_rate": (u - b) / max(1, u), "expected_fp_rate": expected,
                            "filter_bits": m}
+        g48 = E.Graph.from_rows(workload_rows())  # BASELINE cfg 4: Bloom vs exact on the bench graph
+        opts = E.Options(dedup="bloom", max_layer_states=CAP)
+        E.solve(g48, opts)
+        E.timer_begin()
+        r = E.solve(g48, opts)
+        ms = E.timer_end()
+        ex_n = json.loads(r.stats_json)["totals"]["expanded"]
+        out["g48_bloom"] = {"treewidth": r.value, "expanded": ex_n, "ms": ms,
+                            "states_per_s": ex_n / (ms / 1e3),
+                            "path": "partitioned (filter > 2^28 bits): exact bucket dedup, then the "
+                                    "reference's 17-probe filter per distinct child"}
         g40 = E.Graph.from_rows(rows)
         for mode in ("exact", "bloom"):
             E.solve(g40, E.Options(dedup=mode))

@@ -171,7 +171,7 @@ constexpr int tile_slots() { return W == 1 ? 4096 : 2048; }
 template <int W>
 constexpr int tile_set_bytes() { return static_cast<int>(sizeof(TileSet<W, tile_slots<W>()>)); }
 
-template <int W, bool MMW>
+template <int W, bool MMW, bool BLOOM>
 __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __restrict__ P, Control* C,
                                                             Bufs B) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -189,6 +189,28 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
             C->abort = kGrowPartBuf;
         }
         return;
+    }
+    if constexpr (BLOOM) {
+        // partitioned Bloom round: a fresh filter of the reference's size per
+        // round (dp.cpp:93-94), ping-pong by parity; the filter of round r-1
+        // is cleared here for round r+1
+        const u64 m = bloom_bits_for(round_cap(*P, E), P->bpe);
+        if (m / 32 + 1 > B.bloom_cap) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                C->need = m / 32 + 1;
+                C->abort = kGrowBloom;
+            }
+            return;
+        }
+        if (r > 0) {
+            const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+            const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
+            const u64 prev_words = bloom_bits_for(round_cap(*P, C->rs[r - 1].expanded), P->bpe) / 32 + 1;
+            uint4* w4 = reinterpret_cast<uint4*>(B.bloom[(r + 1) & 1]);
+            const u64 n4 = prev_words / 4;
+            for (u64 i = gtid; i < n4; i += gstride) w4[i] = make_uint4(0, 0, 0, 0);
+            for (u64 i = n4 * 4 + gtid; i < prev_words; i += gstride) B.bloom[(r + 1) & 1][i] = 0;
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         C->rs[r].np = pl.np;
@@ -268,8 +290,12 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
 
 constexpr int kPartThreads = 512;
 
-template <int W>
-__global__ void __launch_bounds__(kPartThreads) k_exact_part(Control* C, Bufs B) {
+// BLOOM: the round's distinct keys then meet the reference's Bloom filter
+// (bit positions (h1 + i*h2) mod m, bloom.cpp:86-97), each exactly once, so
+// "any probed bit was clear" is the novelty test; keys the filter calls
+// duplicates (false positives) are dropped as the reference drops them.
+template <int W, bool BLOOM>
+__global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __restrict__ P, Control* C, Bufs B) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int SLOTS = part_slots<W>();
     u64* keys = reinterpret_cast<u64*>(smem_raw);
@@ -339,6 +365,25 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(Control* C, Bufs B)
         for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
             const u64 rank = ranks[i];
             if (rank == ~u64{0}) continue;
+            if constexpr (BLOOM) {
+                Set<W> key;
+#pragma unroll
+                for (int w = 0; w < W; ++w) key.w[w] = keys[W * i + w];
+                const u64 m = bloom_bits_for(round_cap(*P, C->count[r & 1]), P->bpe);
+                unsigned* bits = B.bloom[r & 1];
+                const unsigned h1 = murmur_key<W>(key, kSeed1);
+                const unsigned h2 = murmur_key<W>(key, kSeed2);
+                u64 pos, step;
+                probe_start(h1, h2, m, pos, step);
+                bool novel = false;
+                for (int t = 1; t <= P->hashes; ++t) {
+                    const unsigned bit = 1u << (pos & 31);
+                    novel |= (atomicOr(bits + (pos >> 5), bit) & bit) == 0;
+                    pos += step;
+                    if (pos >= m) pos -= m;
+                }
+                if (!novel) continue;
+            }
             const u64 parent = rank / (64 * W);
             const int v = static_cast<int>(rank % (64 * W));
             atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + parent * W + (v >> 6), u64{1} << (v & 63));
@@ -775,6 +820,7 @@ private:
     int grid_exact_[2] = {0, 0};
     int grid_part_[2] = {0, 0};
     int tile_smem_ = 0;  // 1: scatter launches carry the tile set (ETWG_DEBUG=16)
+    bool part_bloom_ = false;  // Bloom rounds of this decide use scatter/part/append
 
     // Epochs tag look-back statuses (24 bits); on wrap-around the status
     // array is cleared so a status from 2^24 attempts ago cannot match.
@@ -839,11 +885,18 @@ private:
         tile_smem_ = 0;
         if (const char* dbg = std::getenv("ETWG_DEBUG"))
             if (std::atoi(dbg) & 16) tile_smem_ = 1;
-        allow_exact(k_exact_scatter<1, false>, tile_smem_ ? tile_set_bytes<1>() : 0, grid_exact_[0]);
-        allow_exact(k_exact_scatter<2, false>, tile_smem_ ? tile_set_bytes<2>() : 0, grid_exact_[1]);
+        allow_exact(k_exact_scatter<1, false, false>, tile_smem_ ? tile_set_bytes<1>() : 0, grid_exact_[0]);
+        allow_exact(k_exact_scatter<2, false, false>, tile_smem_ ? tile_set_bytes<2>() : 0, grid_exact_[1]);
         int g_mmw[2];
-        allow_exact(k_exact_scatter<1, true>, tile_smem_ ? tile_set_bytes<1>() : 0, g_mmw[0]);
-        allow_exact(k_exact_scatter<2, true>, tile_smem_ ? tile_set_bytes<2>() : 0, g_mmw[1]);
+        allow_exact(k_exact_scatter<1, true, false>, tile_smem_ ? tile_set_bytes<1>() : 0, g_mmw[0]);
+        allow_exact(k_exact_scatter<2, true, false>, tile_smem_ ? tile_set_bytes<2>() : 0, g_mmw[1]);
+        {
+            int g;  // the Bloom variants run on the same grid (same shared memory)
+            allow_exact(k_exact_scatter<1, false, true>, tile_smem_ ? tile_set_bytes<1>() : 0, g);
+            allow_exact(k_exact_scatter<2, false, true>, tile_smem_ ? tile_set_bytes<2>() : 0, g);
+            allow_exact(k_exact_scatter<1, true, true>, tile_smem_ ? tile_set_bytes<1>() : 0, g);
+            allow_exact(k_exact_scatter<2, true, true>, tile_smem_ ? tile_set_bytes<2>() : 0, g);
+        }
         grid_exact_[0] = std::min(grid_exact_[0], g_mmw[0]);
         grid_exact_[1] = std::min(grid_exact_[1], g_mmw[1]);
         if (const char* c = std::getenv("ETWG_SCATTER_CTAS")) {  // CTAs per SM (tuning sweeps)
@@ -859,8 +912,13 @@ private:
                   "occupancy");
             grid = prop.multiProcessorCount * std::max(1, blocks);
         };
-        allow_part(k_exact_part<1>, part_smem_bytes<1>(), grid_part_[0]);
-        allow_part(k_exact_part<2>, part_smem_bytes<2>(), grid_part_[1]);
+        allow_part(k_exact_part<1, false>, part_smem_bytes<1>(), grid_part_[0]);
+        allow_part(k_exact_part<2, false>, part_smem_bytes<2>(), grid_part_[1]);
+        {
+            int g;
+            allow_part(k_exact_part<1, true>, part_smem_bytes<1>(), g);
+            allow_part(k_exact_part<2, true>, part_smem_bytes<2>(), g);
+        }
         check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
         check(cudaMalloc(&d_params_, sizeof(Params)), "malloc params");
         check(cudaMallocHost(&h_params_, sizeof(Params)), "host params");
@@ -1034,7 +1092,7 @@ private:
                 ms += t;
             }
         };
-        if (!exact) {
+        if (!exact && !part_bloom_) {
             if (cfg.use_mmw)
                 timed_launch([&] { k_bloom_dedup<W, true><<<grid_fused_, kThreads, kLocalBytes, stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.insert_ms, prof.t.insert_launches);
@@ -1045,13 +1103,23 @@ private:
                          prof.t.append_ms, prof.t.append_launches);
             return;
         }
+        if (exact)
+            launch_partitioned<W, false>(cfg, timed_launch);
+        else
+            launch_partitioned<W, true>(cfg, timed_launch);
+    }
+
+    // scatter -> part -> append (exact mode, and Bloom mode with a large filter)
+    template <int W, bool BLOOM, typename Launch>
+    void launch_partitioned(const DpConfig& cfg, Launch&& timed_launch) {
+        const int smem = tile_smem_ ? tile_set_bytes<W>() : 0;
         if (cfg.use_mmw)
-            timed_launch([&] { k_exact_scatter<W, true><<<grid_exact_[W - 1], kThreads, tile_smem_ ? tile_set_bytes<W>() : 0, stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_exact_scatter<W, true, BLOOM><<<grid_exact_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
         else
-            timed_launch([&] { k_exact_scatter<W, false><<<grid_exact_[W - 1], kThreads, tile_smem_ ? tile_set_bytes<W>() : 0, stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
-        timed_launch([&] { k_exact_part<W><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_ctl_, b_); },
+        timed_launch([&] { k_exact_part<W, BLOOM><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                      prof.t.insert_ms, prof.t.insert_launches);
         timed_launch([&] { k_append<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
                      prof.t.append_ms, prof.t.append_launches);
@@ -1075,6 +1143,13 @@ private:
         ensure_bloom(u64{1} << 22);
         ensure_claims(u64{1} << 20);
         bloom_round_ = cfg.dedup == DedupMode::bloom;
+        // Bloom filters beyond 2^28 bits (32 MB: random probes stop hitting L2)
+        // take the partitioned path: exact per-bucket dedup in shared memory,
+        // then the filter on each distinct key once (17 probes per distinct
+        // child instead of per offered child)
+        part_bloom_ = bloom_round_ &&
+                      bloom_bits_for(cfg.max_layer_states, cfg.bloom_bits_per_element) > (u64{1} << 28) &&
+                      !(h_params_->flags & 64);
         if (bloom_round_) clean_blooms();
         if (!prof.on) check(cudaEventRecord(ev_[0], stream_), "event");
         auto t0 = std::chrono::steady_clock::now();
@@ -1127,15 +1202,17 @@ private:
     // Grows the structure an aborted round asked for and re-arms the round.
     void grow(Control& c, int W) {
         const unsigned r = c.round;
+        if (bloom_round_) {  // the aborted attempt may have set bits in filter r&1
+            bloom_dirty_[r & 1] = std::max<u64>(
+                bloom_dirty_[r & 1], bloom_bits_for(host_round_cap(c.count[r & 1]), h_params_->bpe) / 32 + 1);
+        }
+        if (std::getenv("ETWG_TRACE"))
+            std::fprintf(stderr, "[engine] round %u abort %u need %llu (E=%llu np=%llu pcap=%llu)\n", r, c.abort,
+                         static_cast<unsigned long long>(c.need), static_cast<unsigned long long>(c.count[r & 1]),
+                         static_cast<unsigned long long>(c.rs[r].np), static_cast<unsigned long long>(c.rs[r].pcap));
         switch (c.abort) {
             case kGrowLayer:
                 ensure_layers(c.need + c.need / 2, static_cast<int>(r & 1), c.count[r & 1]);
-                if (bloom_round_) {  // the aborted attempt left bits in filter r&1
-                    bloom_dirty_[r & 1] = std::max<u64>(
-                        bloom_dirty_[r & 1],
-                        bloom_bits_for(host_round_cap(c.count[r & 1]), h_params_->bpe) / 32);
-                    clean_blooms();
-                }
                 break;
             case kGrowParts:
                 c.part_floor = std::max<u64>(c.part_floor, c.need);
@@ -1158,6 +1235,7 @@ private:
             default:
                 throw DeviceError("device engine: unknown abort code");
         }
+        if (bloom_round_) clean_blooms();
         // re-arm: clear the abort and the partial statistics of round r
         c.abort = kOk;
         c.need = 0;

@@ -280,3 +280,32 @@ def test_bloom_fp_rate_window(E, oracle, gpu):
     probe = [splitmix((1 << 32) + j) for j in range(1_000_000)]
     rate = oracle.bloom_query(bits, m, probe) / len(probe)
     assert 0.3 * 9.838577e-6 <= rate <= 3 * 9.838577e-6
+
+
+def test_partitioned_bloom_large_filter(E, gpu):
+    """Bloom mode with a filter beyond 2^28 bits takes scatter/part/append:
+    exact dedup per bucket, then the reference's filter on each distinct key
+    once. Same verdicts as exact mode; every layer a duplicate-free subset of
+    the exact expansion of its parents; the 2^28-bit fused path (ETWG_DEBUG
+    64 forces it off here) agrees on the verdicts."""
+    rows = G.random_graph(1, 40, 0.3)
+    for k in (21, 22):
+        ex = E.decide(rows, k, dedup="exact", cap=1 << 31)
+        bl = E.decide(rows, k, dedup="bloom", cap=1 << 31)
+        assert bl.outcome == ex.outcome
+        for layer in bl.layers:
+            keys = [s for s, _ in layer]
+            assert len(keys) == len(set(keys))
+        first = [sorted(s for s, _ in x) for x in bl.layers]
+        want = [sorted(s for s, _ in x) for x in ex.layers]
+        for a, b in zip(first, want):
+            if a != b:
+                assert set(a) <= set(b)
+                break
+        # re-expanding a Bloom layer exactly contains the next Bloom layer
+        for r in range(min(4, len(bl.layers) - 1)):
+            nxt = E.expand_layer(rows, k, bl.layers[r], dedup="exact", cap=1 << 31)
+            assert set(s for s, _ in bl.layers[r + 1]) <= set(s for s, _ in nxt.layers[0])
+    g = E.Graph.from_rows(rows)
+    res = E.solve(g, E.Options(dedup="bloom", max_layer_states=1 << 31))
+    assert res.value == 22
