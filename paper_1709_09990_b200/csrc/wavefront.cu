@@ -590,10 +590,18 @@ __device__ __forceinline__ void finish_round(const Params* P, Control* C, const 
     if (emitted == 0 || static_cast<int>(r) + 1 >= P->rounds) C->stop = 1;
 }
 
+// A tile is ITEMS slices of kThreads consecutive parents (slice i = parents
+// tile*span + i*kThreads + t), so one look-back publishes 2048 parents: the
+// look-back chain, not bandwidth, bounded the 256-parent version.
+template <int W>
+constexpr int append_items() { return W == 1 ? 8 : 4; }
+
 template <int W>
 __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ P, Control* C,
                                                      Bufs B) {
     using BlockScan = cub::BlockScan<unsigned, kThreads>;
+    constexpr int ITEMS = append_items<W>();
+    constexpr u64 kSpan = static_cast<u64>(kThreads) * ITEMS;
     __shared__ typename BlockScan::TempStorage scan_tmp;
     __shared__ u64 s_prefix;
     __shared__ u64 s_tile;
@@ -601,7 +609,7 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
     const unsigned r = C->round;
     const unsigned epoch = C->epoch;
     const u64 E = C->count[r & 1];
-    const u64 ntiles = (E + kThreads - 1) / kThreads;
+    const u64 ntiles = (E + kSpan - 1) / kSpan;
     const u64 cap = round_cap(*P, E);
     const u64 limit = cap < B.layer_cap ? cap : B.layer_cap;
     const u64* in = B.keys[r & 1];
@@ -614,22 +622,34 @@ __global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ 
         __syncthreads();
         const u64 tile = s_tile;
         if (tile >= ntiles) break;
-        const u64 idx = tile * kThreads + threadIdx.x;
-        const bool valid = idx < E;
-        const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        const unsigned H = valid ? hin[idx] : 0u;
-        const Set<W> M = valid ? load_set<W>(B.cmask, idx) : Set<W>::zero();
-        const unsigned cnt = static_cast<unsigned>(M.count());
-        unsigned excl_block, total_block;
-        BlockScan(scan_tmp).ExclusiveSum(cnt, excl_block, total_block);
-        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, tile, total_block, epoch);
+        Set<W> S[ITEMS], M[ITEMS];
+        unsigned H[ITEMS], excl[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const u64 idx = tile * kSpan + static_cast<u64>(i) * kThreads + threadIdx.x;
+            const bool valid = idx < E;
+            S[i] = valid ? load_set<W>(in, idx) : Set<W>::zero();
+            H[i] = valid ? hin[idx] : 0u;
+            M[i] = valid ? load_set<W>(B.cmask, idx) : Set<W>::zero();
+        }
+        unsigned total = 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            unsigned slice_total;
+            BlockScan(scan_tmp).ExclusiveSum(static_cast<unsigned>(M[i].count()), excl[i], slice_total);
+            excl[i] += total;
+            total += slice_total;
+            __syncthreads();  // scan_tmp is reused by the next slice
+        }
+        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, tile, total, epoch);
         __syncthreads();
         const u64 prefix = s_prefix;
-        append_survivors<W>(M, S, H, prefix + __shfl_sync(kFull, excl_block, 0), limit, out, hout);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+            append_survivors<W>(M[i], S[i], H[i], prefix + __shfl_sync(kFull, excl[i], 0), limit, out, hout);
         if (threadIdx.x == 0 && tile == ntiles - 1) {
             // the final tile knows the round's survivor total
-            const u64 unique = prefix + total_block;
-            C->rs[r].unique = unique;
+            C->rs[r].unique = prefix + total;
         }
         __syncthreads();
     }
