@@ -166,19 +166,11 @@ __device__ __forceinline__ u64 part_of(const Set<W>& key, int lg) {
     return lg ? slot_hash<W>(key) >> (64 - lg) : 0;
 }
 
-template <int W>
-constexpr int tile_slots() { return W == 1 ? 4096 : 2048; }
-template <int W>
-constexpr int tile_set_bytes() { return static_cast<int>(sizeof(TileSet<W, tile_slots<W>()>)); }
 
 template <int W, bool MMW, bool BLOOM>
 __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __restrict__ P, Control* C,
                                                             Bufs B) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto& ts = *reinterpret_cast<TileSet<W, tile_slots<W>()>*>(smem_raw);
     __shared__ Set<W> adj[64 * W];
-    __shared__ unsigned win[kThreads][2 * W];
-    __shared__ unsigned s_stop;
     if (halted(C)) return;
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
@@ -220,29 +212,23 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
     const Set<W> forbidden = param_set<W>(P->forbidden);
     const u64* in = B.keys[r & 1];
     load_adjacency<W>(P, adj);
-    const u64 ntiles = (E + kThreads - 1) / kThreads;
+    __syncthreads();
+    // warp-granular: no block barrier inside the loop, so a warp whose
+    // parents are cheap never waits for the CTA's slowest warp
+    const u64 nwarps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     u64 offered = 0, pruned = 0, winners = 0;
-    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        if (P->flags & 16) tile_set_clear<W, tile_slots<W>()>(ts);  // launch carries the tile set
-        if (threadIdx.x == 0) s_stop = *reinterpret_cast<volatile unsigned*>(&C->abort);
-        __syncthreads();
-        if (s_stop) break;
-        const u64 idx = tile * kThreads + threadIdx.x;
+    for (u64 base = ((blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5) * 32; base < E;
+         base += nwarps * 32) {
+        if (*reinterpret_cast<volatile unsigned*>(&C->abort)) break;  // warp-uniform read
+        const u64 idx = base + lane;
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
-        if ((P->flags & 32) && valid) {  // timing A/B only: K1 evaluated twice
-            u64 dummy = 0;
-            const Set<W> M2 = candidates<W, MMW>(adj, P->n, P->k, S, forbidden, dummy);
-            if (M2 != M) M = M2;
-        }
+        const Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
         offered += M.count();
-        if (P->flags & 16) tile_dedup<W, tile_slots<W>()>(ts, win, S, M);  // flag 16: A/B only
         winners += M.count();
         if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
         WarpFlat f;
         f.scan(M.count());
-        const u64 warp_base = tile * kThreads + (threadIdx.x & ~31);
         bool full = false;
         for (int t = 0; t < f.total; t += 32) {
             const int j = t + lane;
@@ -259,10 +245,10 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
                 if (slot < pl.cap) {
                     u64* rec = B.recs + (part * pl.cap + slot) * rec_words<W>();
                     if constexpr (W == 1) {
-                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(warp_base + src, v));
+                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(base + src, v));
                     } else {
                         *reinterpret_cast<ulonglong4*>(rec) =
-                            make_ulonglong4(key.w[0], key.w[1], child_rank<W>(warp_base + src, v), 0);
+                            make_ulonglong4(key.w[0], key.w[1], child_rank<W>(base + src, v), 0);
                     }
                 } else {
                     full = true;
@@ -273,7 +259,6 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
             C->need = 2 * pl.cap;
             C->abort = kGrowRecs;
         }
-        __syncthreads();
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -838,8 +823,8 @@ private:
     bool bloom_round_ = false;    // current decide runs the fused Bloom round
     int grid_fused_ = 0;
     int grid_exact_[2] = {0, 0};
+    int grid_exact_mmw_[2] = {0, 0};
     int grid_part_[2] = {0, 0};
-    int tile_smem_ = 0;  // 1: scatter launches carry the tile set (ETWG_DEBUG=16)
     bool part_bloom_ = false;  // Bloom rounds of this decide use scatter/part/append
 
     // Epochs tag look-back statuses (24 bits); on wrap-around the status
@@ -900,30 +885,22 @@ private:
             check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, bytes), "occupancy");
             grid = prop.multiProcessorCount * std::max(1, blocks);
         };
-        // the tile set is only used by the ETWG_DEBUG=16 A/B; the default launch
-        // takes no dynamic shared memory and the occupancy that allows
-        tile_smem_ = 0;
-        if (const char* dbg = std::getenv("ETWG_DEBUG"))
-            if (std::atoi(dbg) & 16) tile_smem_ = 1;
-        allow_exact(k_exact_scatter<1, false, false>, tile_smem_ ? tile_set_bytes<1>() : 0, grid_exact_[0]);
-        allow_exact(k_exact_scatter<2, false, false>, tile_smem_ ? tile_set_bytes<2>() : 0, grid_exact_[1]);
-        int g_mmw[2];
-        allow_exact(k_exact_scatter<1, true, false>, tile_smem_ ? tile_set_bytes<1>() : 0, g_mmw[0]);
-        allow_exact(k_exact_scatter<2, true, false>, tile_smem_ ? tile_set_bytes<2>() : 0, g_mmw[1]);
+        allow_exact(k_exact_scatter<1, false, false>, 0, grid_exact_[0]);
+        allow_exact(k_exact_scatter<2, false, false>, 0, grid_exact_[1]);
+        allow_exact(k_exact_scatter<1, true, false>, 0, grid_exact_mmw_[0]);
+        allow_exact(k_exact_scatter<2, true, false>, 0, grid_exact_mmw_[1]);
         {
-            int g;  // the Bloom variants run on the same grid (same shared memory)
-            allow_exact(k_exact_scatter<1, false, true>, tile_smem_ ? tile_set_bytes<1>() : 0, g);
-            allow_exact(k_exact_scatter<2, false, true>, tile_smem_ ? tile_set_bytes<2>() : 0, g);
-            allow_exact(k_exact_scatter<1, true, true>, tile_smem_ ? tile_set_bytes<1>() : 0, g);
-            allow_exact(k_exact_scatter<2, true, true>, tile_smem_ ? tile_set_bytes<2>() : 0, g);
+            // the Bloom variants run on the grid of their exact twin, capped by their own residency
+            int g;
+            allow_exact(k_exact_scatter<1, false, true>, 0, g);
+            grid_exact_[0] = std::min(grid_exact_[0], g);
+            allow_exact(k_exact_scatter<2, false, true>, 0, g);
+            grid_exact_[1] = std::min(grid_exact_[1], g);
+            allow_exact(k_exact_scatter<1, true, true>, 0, g);
+            grid_exact_mmw_[0] = std::min(grid_exact_mmw_[0], g);
+            allow_exact(k_exact_scatter<2, true, true>, 0, g);
+            grid_exact_mmw_[1] = std::min(grid_exact_mmw_[1], g);
         }
-        grid_exact_[0] = std::min(grid_exact_[0], g_mmw[0]);
-        grid_exact_[1] = std::min(grid_exact_[1], g_mmw[1]);
-        if (const char* c = std::getenv("ETWG_SCATTER_CTAS")) {  // CTAs per SM (tuning sweeps)
-            const int per = std::atoi(c);
-            for (int w = 0; w < 2; ++w) grid_exact_[w] = std::min(grid_exact_[w], prop.multiProcessorCount * per);
-        }
-        if (tile_smem_) tile_smem_ = 1;
         auto allow_part = [&](auto kernel, int bytes, int& grid) {
             check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                   "smem attribute");
@@ -1132,9 +1109,9 @@ private:
     // scatter -> part -> append (exact mode, and Bloom mode with a large filter)
     template <int W, bool BLOOM, typename Launch>
     void launch_partitioned(const DpConfig& cfg, Launch&& timed_launch) {
-        const int smem = tile_smem_ ? tile_set_bytes<W>() : 0;
+        const int smem = 0;
         if (cfg.use_mmw)
-            timed_launch([&] { k_exact_scatter<W, true, BLOOM><<<grid_exact_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_exact_scatter<W, true, BLOOM><<<grid_exact_mmw_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
         else
             timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q --timeout 600 2>&1 | tail -2
-timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | sed -n 2p
-timeout 600 python tools/prof_g48.py exact 2>&1 | head -8
+timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q --timeout 600 2>&1 | tail -1
+for c in 4 5 6; do echo "ctas $c"; ETWG_SCATTER_CTAS=$c timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | sed -n 2p; done
+timeout 600 python tools/prof_g48.py exact 2>&1 | head -6
