@@ -31,6 +31,8 @@
 // round's growth and re-runs a round whose buckets overflowed.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+
+#include <cub/block/block_scan.cuh>
 #include <nccl.h>
 
 #include <algorithm>
@@ -90,7 +92,8 @@ struct ShardRound {
 struct ShardCtl {
     u64 count[2];  // local layer sizes, ping-pong by round parity
     unsigned round, stop, epoch, pad;
-    u64 ticket;  // owner-pass partition ticket
+    u64 ticket;   // owner-pass partition ticket
+    u64 ticket2;  // compaction tile ticket
     ShardStat mine;
     ShardStat all[kMaxShards];
     ShardRound rs[kMaxRounds];
@@ -120,8 +123,12 @@ struct ShardBufs {
     // of one device, and a shard's records for itself — no copy)
     const u64* src_recs[kMaxShards];
     const unsigned* src_cnt[kMaxShards];
-    u64* tiles;          // look-back status per partition
+    u64* tiles;          // look-back status per compaction tile (256 partitions)
     u64 tile_cap;
+    u64* stage;          // owner output staging: [partition][owner_slots] keys
+    unsigned* stage_hist;
+    unsigned* pcount;    // survivors per partition
+    u64 stage_cap;       // partitions the staging holds
     unsigned* bloom;     // the owner's Bloom slice (32-bit words)
     u64 bloom_cap;       // words
 };
@@ -283,12 +290,8 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
     u64* keys = reinterpret_cast<u64*>(vals + SLOTS);
     u64* sortk = keys + SLOTS * W;
     __shared__ unsigned s_full, s_cnt;
-    __shared__ u64 s_part, s_prefix;
+    __shared__ u64 s_part;
     if (C->stop) return;
-    const unsigned r = C->round;
-    const unsigned epoch = C->epoch;
-    u64* out = B.keys[(r + 1) & 1];
-    unsigned* hout = B.hist[(r + 1) & 1];
     for (;;) {
         if (threadIdx.x == 0) s_part = atomicAdd(&C->ticket, 1ull);
         __syncthreads();
@@ -374,30 +377,82 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
                 __syncthreads();
             }
         }
-        // every claimed partition publishes its count, even an aborted one
-        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, part, cnt, epoch);
-        __syncthreads();
-        const u64 prefix = s_prefix;
+        // sorted survivors to the partition's staging slot; k_owner_compact
+        // places them (no look-back chain between partitions here)
+        u64* stage = B.stage + part * SLOTS * W;
+        unsigned* shist = B.stage_hist + part * SLOTS;
         for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
-            const u64 pos = prefix + i;
-            if (pos >= B.layer_cap) break;
             const int slot = static_cast<int>(sortk[i] & 0xFFF);
-            Set<W> key;
 #pragma unroll
-            for (int w = 0; w < W; ++w) key.w[w] = keys[W * slot + w];
-            store_set<W>(out, pos, key);
-            hout[pos] = static_cast<unsigned>(vals[slot].y);
+            for (int w = 0; w < W; ++w) stage[W * i + w] = keys[W * slot + w];
+            shist[i] = static_cast<unsigned>(vals[slot].y);
         }
         if (threadIdx.x == 0) {
+            B.pcount[part] = cnt;
             if (full) {
                 atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortParts));
                 atomicMax(&C->mine.need_parts, 2 * pl.np);
             }
-            if (prefix + cnt > B.layer_cap) {
-                atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortLayer));
-                atomicMax(&C->mine.need_layer, prefix + cnt);
+        }
+        __syncthreads();
+    }
+}
+
+// Partition survivors -> the contiguous next layer: tiles of 256
+// partitions, block scan of their counts, one decoupled look-back per tile,
+// then each warp copies its partitions' staged states (coalesced).
+template <int W>
+__global__ void __launch_bounds__(kRouteThreads) k_owner_compact(ShardCtl* C, ShardBufs B, Plan pl) {
+    using BlockScan = cub::BlockScan<unsigned, kRouteThreads>;
+    constexpr int SLOTS = owner_slots<W>();
+    __shared__ typename BlockScan::TempStorage scan_tmp;
+    __shared__ unsigned s_excl[kRouteThreads], s_cnt[kRouteThreads];
+    __shared__ u64 s_prefix, s_tile;
+    if (C->stop) return;
+    const unsigned r = C->round;
+    const unsigned epoch = C->epoch;
+    u64* out = B.keys[(r + 1) & 1];
+    unsigned* hout = B.hist[(r + 1) & 1];
+    const u64 ntiles = (pl.np + kRouteThreads - 1) / kRouteThreads;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&C->ticket2, 1ull);
+        __syncthreads();
+        const u64 tile = s_tile;
+        if (tile >= ntiles) break;
+        const u64 part = tile * kRouteThreads + threadIdx.x;
+        const unsigned cnt = part < pl.np ? B.pcount[part] : 0u;
+        unsigned excl, total;
+        BlockScan(scan_tmp).ExclusiveSum(cnt, excl, total);
+        s_excl[threadIdx.x] = excl;
+        s_cnt[threadIdx.x] = cnt;
+        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, tile, total, epoch);
+        __syncthreads();
+        const u64 prefix = s_prefix;
+        for (int j = warp; j < kRouteThreads; j += kRouteThreads / 32) {
+            const u64 p = tile * kRouteThreads + j;
+            if (p >= pl.np) break;
+            const unsigned c = s_cnt[j];
+            const u64 base = prefix + s_excl[j];
+            const u64* stage = B.stage + p * SLOTS * W;
+            const unsigned* shist = B.stage_hist + p * SLOTS;
+            for (unsigned i = lane; i < c; i += 32) {
+                const u64 pos = base + i;
+                if (pos >= B.layer_cap) break;
+                Set<W> key;
+#pragma unroll
+                for (int w = 0; w < W; ++w) key.w[w] = stage[W * i + w];
+                store_set<W>(out, pos, key);
+                hout[pos] = shist[i];
             }
-            if (part == pl.np - 1) C->mine.unique = prefix + cnt;
+        }
+        if (threadIdx.x == 0 && tile == ntiles - 1) {
+            const u64 unique = prefix + total;
+            C->mine.unique = unique;
+            if (unique > B.layer_cap) {
+                atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortLayer));
+                atomicMax(&C->mine.need_layer, unique);
+            }
         }
         __syncthreads();
     }
@@ -439,6 +494,7 @@ __global__ void k_shard_finish(const Params* __restrict__ P, ShardCtl* C, Plan p
     C->round = r + 1;
     C->epoch = (C->epoch & kEpochMask) == kEpochMask ? 1 : C->epoch + 1;
     C->ticket = 0;
+    C->ticket2 = 0;
     C->mine = ShardStat{};
     if (emitted == 0 || static_cast<int>(r) + 1 >= pl.rounds) C->stop = 1;
 }
@@ -509,6 +565,7 @@ struct Shard {
     ShardBufs b{};
     u64 bloom_dirty = 0;  // words of the Bloom slice that may hold bits
     int box_words = 0;    // W the boxes were sized for
+    int stage_words = 0;  // W the owner staging was sized for
 };
 
 class ShardSet {
@@ -634,6 +691,7 @@ public:
             for (Shard& s : local_) launch_route(s, pl, W, cfg.use_mmw);
             exchange(pl, W);
             for (Shard& s : local_) launch_owner(s, pl, W, bloom);
+            for (Shard& s : local_) launch_compact(s, pl, W);
             allgather_stats();
             for (Shard& s : local_) {
                 Plan p = pl;
@@ -837,6 +895,9 @@ private:
         cudaFree(s.b.in_cnt);
         cudaFree(s.b.tiles);
         cudaFree(s.b.bloom);
+        cudaFree(s.b.stage);
+        cudaFree(s.b.stage_hist);
+        cudaFree(s.b.pcount);
         s = Shard{};
     }
 
@@ -980,6 +1041,22 @@ private:
             if (comm_) check(cudaMalloc(&s.b.in_cnt, cap * 4), "inbox counts");
             s.b.cnt_cap = cap;
         }
+        if (pl.np > s.b.stage_cap || !s.b.stage) {
+            const u64 cap = std::max<u64>(pl.np + pl.np / 4, 64);
+            cudaFree(s.b.stage);
+            cudaFree(s.b.stage_hist);
+            cudaFree(s.b.pcount);
+            check(cudaMalloc(&s.b.stage, cap * owner_slots<1>() * 8 * W), "owner staging");
+            check(cudaMalloc(&s.b.stage_hist, cap * owner_slots<1>() * 4), "owner staging");
+            check(cudaMalloc(&s.b.pcount, cap * 4), "partition counts");
+            s.b.stage_cap = cap;
+            s.stage_words = W;
+        }
+        if (W != s.stage_words) {  // staging sized for one-word keys: regrow at the new width
+            cudaFree(s.b.stage);
+            check(cudaMalloc(&s.b.stage, s.b.stage_cap * owner_slots<1>() * 8 * W), "owner staging");
+            s.stage_words = W;
+        }
         if (pl.np + 1 > s.b.tile_cap || !s.b.tiles) {
             const u64 cap = std::max<u64>((pl.np + 1) * 2, u64{1} << 12);
             cudaFree(s.b.tiles);
@@ -1057,6 +1134,19 @@ private:
         ++launches_;
     }
 
+    void launch_compact(Shard& s, const Plan& pl, int W) {
+        Plan p = pl;
+        p.me = s.me;
+        const int grid = std::max(1, std::min<int>(static_cast<int>((pl.np + kRouteThreads - 1) / kRouteThreads),
+                                                   grid_route_[0]));
+        if (W == 1)
+            k_owner_compact<1><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
+        else
+            k_owner_compact<2><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
+        check(cudaGetLastError(), "compact launch");
+        ++launches_;
+    }
+
     // outbox block d of shard s -> inbox slot s of shard d (NCCL); virtual
     // shards and a shard's own block are read in place by k_owner
     void exchange(const Plan& pl, int W) {
@@ -1094,6 +1184,7 @@ private:
     void rearm(Shard& s) {
         ShardCtl& c = *s.h_ctl;
         c.ticket = 0;
+        c.ticket2 = 0;
         c.mine = ShardStat{};
         c.epoch = next_epoch(s, c.epoch);
         check(cudaMemcpyAsync(s.d_ctl, s.h_ctl, offsetof(ShardCtl, all), cudaMemcpyHostToDevice, stream_), "re-arm");
