@@ -97,13 +97,18 @@ ELIMTW_API void etwg_reset_times(void);
  *                                one shard per process over NCCL; every rank
  *                                must then make the same sequence of solves
  *   etwg_shard_release()         back to the single-device engine
- *   etwg_shard_info              world size, rank, 1 when virtual            */
+ *   etwg_shard_info              world size, rank, 1 when virtual
+ *   etwg_shard_exchange_p2p      1 when owners pull records over NVLink     */
 ELIMTW_API etw_status etwg_set_virtual_shards(int shards, char* err, size_t err_len);
 ELIMTW_API etw_status etwg_nccl_unique_id(uint8_t* id128, char* err, size_t err_len);
 ELIMTW_API etw_status etwg_shard_init(const uint8_t* id128, int rank, int world, int device, char* err,
                                       size_t err_len);
 ELIMTW_API void etwg_shard_release(void);
 ELIMTW_API void etwg_shard_info(int* world, int* rank, int* is_virtual);
+/* 1 when the NCCL path's owners read their peers' outboxes over NVLink
+ * (CUDA IPC; ETWG_EXCHANGE=nccl or a failed peer mapping selects NCCL
+ * grouped send/recv instead) */
+ELIMTW_API int etwg_shard_exchange_p2p(void);
 
 /* host preprocessing (no GPU needed); rows as above */
 ELIMTW_API void etwg_graph_rows(const etw_graph* g, uint64_t* rows);

@@ -472,6 +472,14 @@ void etwg_shard_release(void) {
     }
 }
 
+int etwg_shard_exchange_p2p(void) {
+    try {
+        return shard_p2p();
+    } catch (...) {
+        return 0;
+    }
+}
+
 void etwg_shard_info(int* world, int* rank, int* is_virtual) {
     try {
         shard_info(world, rank, is_virtual);

@@ -130,6 +130,7 @@ void shard_unique_id(unsigned char* out128);
 void shard_init_nccl(const unsigned char* id128, int rank, int world, int device);
 void shard_release();
 void shard_info(int* world, int* rank, int* virt);
+int shard_p2p();  // 1 when the NCCL path pulls records over NVLink (CUDA IPC)
 void shard_timer_begin();
 double shard_timer_end();
 void shard_accumulate(KernelTimes& t);

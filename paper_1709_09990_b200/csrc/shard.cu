@@ -606,9 +606,15 @@ public:
         rank_ = rank;
         local_.resize(1);
         create_shard(local_[0], rank);
+        // owners pull their buckets from the peers' outboxes over NVLink
+        // (CUDA IPC) unless ETWG_EXCHANGE=nccl or a peer mapping fails
+        const char* ex = std::getenv("ETWG_EXCHANGE");
+        p2p_ = world > 1 && !(ex && std::strcmp(ex, "nccl") == 0);
+        handles_dirty_ = true;
     }
 
     void release() {
+        close_peers();
         for (Shard& s : local_) destroy_shard(s);
         local_.clear();
         if (comm_) {
@@ -618,6 +624,10 @@ public:
         G_ = 1;
         rank_ = 0;
     }
+
+    // exchange mode of the NCCL path: 1 = owners read peers' outboxes over
+    // NVLink (CUDA IPC), 0 = NCCL grouped send/recv of the outbox blocks
+    int p2p() const { return p2p_ ? 1 : 0; }
 
     void info(int* world, int* rank, int* virt) const {
         if (world) *world = G_;
@@ -688,6 +698,11 @@ public:
             for (u64 c : count)
                 if (c >> 32) throw DeviceError("sharded layer slice exceeds 2^32 states");
             for (Shard& s : local_) prepare_round(s, pl, W, bloom, count);
+            if (comm_ && p2p_ && handles_dirty_) {
+                share_outboxes(local_[0]);
+                if (!p2p_)  // a peer mapping failed on some rank: NCCL exchange from here on
+                    for (Shard& s : local_) prepare_round(s, pl, W, bloom, count);
+            }
             for (Shard& s : local_) launch_route(s, pl, W, cfg.use_mmw);
             exchange(pl, W);
             for (Shard& s : local_) launch_owner(s, pl, W, bloom);
@@ -814,6 +829,11 @@ private:
     bool trace_ = std::getenv("ETWG_SHARD_TRACE") != nullptr;
     u64* d_wit_ = nullptr;
     int pl_round_parity_ = 0;  // buffer holding the current round's input layer
+    bool p2p_ = false;          // NCCL mode: pull records over NVLink instead of send/recv
+    bool handles_dirty_ = false;  // outboxes (re)allocated since the last handle exchange
+    const u64* peer_out_[kMaxShards] = {};
+    const unsigned* peer_cnt_[kMaxShards] = {};
+    unsigned char* d_handles_ = nullptr;
 
     void init_device(int dev) {
         if (device_ == dev && stream_) return;
@@ -1029,8 +1049,9 @@ private:
             cudaFree(s.b.in);
             s.b.in = nullptr;
             check(cudaMalloc(&s.b.out, cap * 8 * (W + 1)), "outbox");
-            if (comm_) check(cudaMalloc(&s.b.in, cap * 8 * (W + 1)), "inbox");
+            if (comm_ && !p2p_) check(cudaMalloc(&s.b.in, cap * 8 * (W + 1)), "inbox");
             s.b.box_cap = cap;
+            handles_dirty_ = true;
         }
         if (cnts > s.b.cnt_cap || !s.b.out_cnt) {
             const u64 cap = std::max<u64>(cnts * 2, u64{1} << 12);
@@ -1038,8 +1059,9 @@ private:
             cudaFree(s.b.in_cnt);
             s.b.in_cnt = nullptr;
             check(cudaMalloc(&s.b.out_cnt, cap * 4), "outbox counts");
-            if (comm_) check(cudaMalloc(&s.b.in_cnt, cap * 4), "inbox counts");
+            if (comm_ && !p2p_) check(cudaMalloc(&s.b.in_cnt, cap * 4), "inbox counts");
             s.b.cnt_cap = cap;
+            handles_dirty_ = true;
         }
         if (pl.np > s.b.stage_cap || !s.b.stage) {
             const u64 cap = std::max<u64>(pl.np + pl.np / 4, 64);
@@ -1118,6 +1140,9 @@ private:
             } else if (src == s.me) {
                 s.b.src_recs[src] = s.b.out + s.me * block;
                 s.b.src_cnt[src] = s.b.out_cnt + s.me * pl.np;
+            } else if (p2p_) {  // the peer's outbox, read over NVLink
+                s.b.src_recs[src] = peer_out_[src] + s.me * block;
+                s.b.src_cnt[src] = peer_cnt_[src] + s.me * pl.np;
             } else {
                 s.b.src_recs[src] = s.b.in + src * block;
                 s.b.src_cnt[src] = s.b.in_cnt + src * pl.np;
@@ -1151,6 +1176,16 @@ private:
     // shards and a shard's own block are read in place by k_owner
     void exchange(const Plan& pl, int W) {
         if (!comm_) return;
+        if (p2p_) {
+            // every route must be complete before any owner reads a peer's
+            // outbox: a stream-ordered allgather of the route counters is the
+            // barrier (the post-owner allgather refreshes all[] anyway)
+            Nccl& nc = Nccl::get();
+            Shard& s = local_[0];
+            nc.check(nc.AllGather(&s.d_ctl->mine, &s.d_ctl->all[0], sizeof(ShardStat), ncclUint8, comm_, stream_),
+                     "route barrier");
+            return;
+        }
         const u64 block = pl.np * pl.cap * (W + 1);
         const u64 bytes = block * 8, cnt_bytes = pl.np * 4;
         Nccl& nc = Nccl::get();
@@ -1178,6 +1213,71 @@ private:
         Shard& s = local_[0];
         nc.check(nc.AllGather(&s.d_ctl->mine, &s.d_ctl->all[0], sizeof(ShardStat), ncclUint8, comm_, stream_),
                  "allgather stats");
+    }
+
+    // Collective: every rank publishes CUDA IPC handles of its outbox and
+    // bucket counts and maps its peers'. If any rank fails to map, all fall
+    // back to the NCCL send/recv exchange.
+    struct IpcRecord {
+        cudaIpcMemHandle_t out, cnt;
+        int ok, pad[3];
+    };
+
+    void share_outboxes(Shard& s) {
+        close_peers();
+        Nccl& nc = Nccl::get();
+        const size_t rec = sizeof(IpcRecord);
+        if (!d_handles_) check(cudaMalloc(&d_handles_, rec * kMaxShards + 64), "ipc handles");
+        std::vector<IpcRecord> h(G_);
+        IpcRecord mine{};
+        mine.ok = cudaIpcGetMemHandle(&mine.out, s.b.out) == cudaSuccess &&
+                  cudaIpcGetMemHandle(&mine.cnt, s.b.out_cnt) == cudaSuccess;
+        cudaGetLastError();
+        check(cudaMemcpyAsync(d_handles_ + rec * s.me, &mine, rec, cudaMemcpyHostToDevice, stream_), "ipc h2d");
+        nc.check(nc.AllGather(d_handles_ + rec * s.me, d_handles_, rec, ncclUint8, comm_, stream_), "ipc allgather");
+        check(cudaMemcpyAsync(h.data(), d_handles_, rec * G_, cudaMemcpyDeviceToHost, stream_), "ipc d2h");
+        check(cudaStreamSynchronize(stream_), "ipc sync");
+        int ok = 1;
+        for (int p = 0; p < G_; ++p) ok &= h[p].ok;
+        for (int p = 0; ok && p < G_; ++p) {
+            if (p == s.me) continue;
+            void* a = nullptr;
+            void* b = nullptr;
+            if (cudaIpcOpenMemHandle(&a, h[p].out, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+                cudaIpcOpenMemHandle(&b, h[p].cnt, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                if (a) cudaIpcCloseMemHandle(a);
+                ok = 0;
+                break;
+            }
+            peer_out_[p] = static_cast<const u64*>(a);
+            peer_cnt_[p] = static_cast<const unsigned*>(b);
+        }
+        // agree: p2p only if every rank mapped every peer
+        int* flags = reinterpret_cast<int*>(d_handles_);
+        check(cudaMemcpyAsync(flags + s.me, &ok, sizeof(int), cudaMemcpyHostToDevice, stream_), "ipc flag");
+        nc.check(nc.AllGather(flags + s.me, flags, sizeof(int), ncclUint8, comm_, stream_), "ipc flag allgather");
+        std::vector<int> all(G_);
+        check(cudaMemcpyAsync(all.data(), flags, sizeof(int) * G_, cudaMemcpyDeviceToHost, stream_), "ipc flag d2h");
+        check(cudaStreamSynchronize(stream_), "ipc sync");
+        for (int v : all) ok &= v;
+        handles_dirty_ = false;
+        if (!ok) {
+            close_peers();
+            p2p_ = false;
+            s.b.box_cap = 0;  // reallocate with inboxes for the NCCL exchange
+            s.b.cnt_cap = 0;
+            std::fprintf(stderr, "[elimtw] CUDA IPC peer mapping unavailable: NCCL send/recv exchange\n");
+        }
+    }
+
+    void close_peers() {
+        for (int p = 0; p < kMaxShards; ++p) {
+            if (peer_out_[p]) cudaIpcCloseMemHandle(const_cast<u64*>(peer_out_[p]));
+            if (peer_cnt_[p]) cudaIpcCloseMemHandle(const_cast<unsigned*>(peer_cnt_[p]));
+            peer_out_[p] = nullptr;
+            peer_cnt_[p] = nullptr;
+        }
     }
 
     // re-arm an aborted round: counters cleared, new look-back epoch
@@ -1277,6 +1377,12 @@ void shard_info(int* world, int* rank, int* virt) {
     ShardSet& s = ShardSet::instance();
     std::lock_guard<std::mutex> lock(s.mu);
     s.info(world, rank, virt);
+}
+
+int shard_p2p() {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    return s.p2p();
 }
 
 void shard_timer_begin() {

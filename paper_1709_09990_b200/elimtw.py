@@ -122,6 +122,7 @@ def library() -> C.CDLL:
         "etwg_shard_init": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
         "etwg_shard_release": (None, []),
         "etwg_shard_info": (None, [_ip, _ip, _ip]),
+        "etwg_shard_exchange_p2p": (C.c_int, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -488,7 +489,8 @@ def shard_release() -> None:
 def shard_info() -> dict:
     w, r, v = C.c_int(), C.c_int(), C.c_int()
     library().etwg_shard_info(C.byref(w), C.byref(r), C.byref(v))
-    return {"world": w.value, "rank": r.value, "virtual": bool(v.value)}
+    return {"world": w.value, "rank": r.value, "virtual": bool(v.value),
+            "p2p": bool(library().etwg_shard_exchange_p2p())}
 
 
 # host preprocessing (no device needed)

@@ -184,7 +184,7 @@ def test_nccl_one_rank_communicator(E, gpu):
     want = {k: E.decide(rows, k, dedup="exact") for k in (21, 22)}
     E.shard_init(E.nccl_unique_id(), 0, 1, gpu["device"])
     try:
-        assert E.shard_info() == {"world": 1, "rank": 0, "virtual": False}
+        assert E.shard_info() == {"world": 1, "rank": 0, "virtual": False, "p2p": False}
         for k, w in want.items():
             got = E.decide(rows, k, dedup="exact")
             assert got.outcome == w.outcome
