@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
     auto& ts = *reinterpret_cast<TileSet<W, route_tile_slots<W>()>*>(smem_raw);
     __shared__ Set<W> adj[64 * W];
     __shared__ unsigned win[kRouteThreads][2 * W];
+    __shared__ unsigned mmw_keep[MMW ? kRouteThreads : 1][2 * W];
     if (C->stop) return;
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
         const unsigned H = valid ? hin[idx] : 0u;
-        Set<W> M = valid ? candidates<W, MMW, true>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
+        Set<W> M = warp_candidates<W, MMW, true>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         offered += M.count();
         if constexpr (TILE) {
             tile_set_clear<W, route_tile_slots<W>()>(ts);

@@ -250,33 +250,74 @@ __device__ __forceinline__ Set<W> reach_from(const Set<W>* adj, const Set<W>& S,
 }
 
 // Minor-min-width on eliminate(G, S + v) (init_view_after, mmw.cpp:20-43,
-// then the shared contraction loop of mmw.hpp). rows[w] = Q(S,w) for every
-// w outside S. Returns early once the bound exceeds cap.
+// then run_mmw / contract_step, mmw.cpp:81-140) with the minor held
+// explicitly as bitmask rows: nb[w] starts as Q(S+v, w) — rows[w], plus
+// rows[v] when w is in it — and a contraction of (x, u) is one mask union
+// plus |N(u)| row edits, instead of the shared contraction loop's DFS
+// through eliminated vertices per step. Same choices as the reference:
+// min degree, smallest index on ties; its min-degree neighbour, smallest
+// index on ties; degree-0 classes dropped; degrees updated by
+// deg[x] + deg[u] - c - 2 and -1 for the c common neighbours. Returns
+// early once the bound exceeds cap.
 template <int W>
-__device__ int mmw_child(const Set<W>* adj, int n, int cap, const Set<W>& S, int v,
-                         const Set<W>* rows) {
+__device__ int mmw_child(int n, int cap, const Set<W>& S, int v, const Set<W>* rows) {
     constexpr int N = 64 * W;
-    unsigned char parent[N];
-    unsigned char degree[N];
-    MinorState<W> m{adj, S, Set<W>::zero(), parent, degree};
-    m.elim.add(v);
-    m.alive = Set<W>::prefix(n) - m.elim;
-    for (int x = 0; x < n; ++x) {
-        parent[x] = static_cast<unsigned char>(x);
-        degree[x] = 0;
+    Set<W> nb[N];
+    unsigned char deg[N];
+    Set<W> alive = Set<W>::prefix(n) - S;
+    alive.del(v);
+    const Set<W> rv = rows[v];
+    for (int w : members(alive)) {
+        Set<W> a = rows[w];
+        if (rv.has(w)) a |= rv;  // eliminating v joins Q(S,v) into a clique
+        a.del(v);
+        a.del(w);
+        nb[w] = a;
+        deg[w] = static_cast<unsigned char>(a.count());
     }
-    // eliminating v turns Q(S,v) into a clique; everyone else keeps Q(S,w)
-    for (int w : members(m.alive)) {
-        if (rows[v].has(w)) {
-            Set<W> j = rows[w] | rows[v];
-            j.del(v);
-            j.del(w);
-            degree[w] = static_cast<unsigned char>(j.count());
-        } else {
-            degree[w] = static_cast<unsigned char>(rows[w].count());
+    int bound = 0;
+    while (alive.count() >= 2) {
+        int d1 = 1 << 30, d2 = 1 << 30, x1 = -1;
+        for (int x : members(alive)) {
+            const int d = deg[x];
+            if (d < d1) {
+                d2 = d1;
+                d1 = d;
+                x1 = x;
+            } else if (d < d2) {
+                d2 = d;
+            }
         }
+        if (d2 > bound) bound = d2;
+        if (bound > cap) return bound;
+        if (d1 == 0) {  // isolated class: drop it
+            alive.del(x1);
+            continue;
+        }
+        int u = -1, du = 1 << 30;
+        for (int x : members(nb[x1])) {
+            if (deg[x] < du) {
+                du = deg[x];
+                u = x;
+            }
+        }
+        const Set<W> nu = nb[u];
+        const Set<W> common = nb[x1] & nu;
+        Set<W> merged = nb[x1] | nu;
+        merged.del(x1);
+        merged.del(u);
+        nb[x1] = merged;
+        deg[x1] = static_cast<unsigned char>(deg[x1] + deg[u] - common.count() - 2);
+        alive.del(u);
+        Set<W> moved = nu;
+        moved.del(x1);
+        for (int x : members(moved)) {
+            nb[x].del(u);
+            nb[x].add(x1);
+        }
+        for (int x : members(common)) --deg[x];
     }
-    return minor_min_width<W>(m, cap);
+    return bound;
 }
 
 template <int W, bool MMW, bool COMPACT = false>
@@ -299,7 +340,7 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
         for (int w : members(open)) rows[w] = reach_from<W, COMPACT>(adj, S, R, w);
         for (int v : members(eligible)) {
             if (rows[v].count() > k) continue;
-            if (mmw_child<W>(adj, n, k, S, v, rows) > k) {
+            if (mmw_child<W>(n, k, S, v, rows) > k) {
                 ++pruned;
                 continue;
             }
@@ -307,6 +348,56 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
         }
     }
     return keep;
+}
+
+// Warp-collective candidate evaluation (call with all 32 lanes; `valid`
+// marks lanes holding a parent). The degree test runs per parent; with MMW
+// the surviving children are then flattened across the warp so each lane
+// evaluates the minor-min-width bound of one child (dp.cpp:57-63) — a
+// parent's children no longer run serially in one thread, which is what
+// bounded small MMW layers. `scratch` is a per-thread row of 2W words in
+// shared memory.
+template <int W, bool MMW, bool COMPACT = false>
+__device__ __forceinline__ Set<W> warp_candidates(const Set<W>* adj, int n, int k, const Set<W>& S, bool valid,
+                                                  const Set<W>& forbidden, u64& pruned,
+                                                  unsigned (*scratch)[2 * W]) {
+    u64 unused = 0;
+    Set<W> M = valid ? candidates<W, false, COMPACT>(adj, n, k, S, forbidden, unused) : Set<W>::zero();
+    if constexpr (!MMW) {
+        return M;
+    } else {
+        constexpr int N = 64 * W;
+        const int lane = threadIdx.x & 31;
+        const int wslot = threadIdx.x & ~31;
+#pragma unroll
+        for (int i = 0; i < 2 * W; ++i) scratch[threadIdx.x][i] = 0;
+        __syncwarp();
+        WarpFlat f;
+        f.scan(M.count());
+        for (int t = 0; t < f.total; t += 32) {
+            const int j = t + lane;
+            const int src = f.source(j);
+            const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
+            const Set<W> Ms = shfl_set<W>(M, src);
+            const Set<W> Ss = shfl_set<W>(S, src);
+            if (j < f.total) {
+                const int v = nth_member<W>(Ms, j - excl);
+                Set<W> R[N], rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
+                component_reach<W, COMPACT>(adj, Ss, R);
+                for (int w : members(Set<W>::prefix(n) - Ss)) rows[w] = reach_from<W, COMPACT>(adj, Ss, R, w);
+                if (mmw_child<W>(n, k, Ss, v, rows) > k)
+                    ++pruned;
+                else
+                    atomicOr(&scratch[wslot + src][v >> 5], 1u << (v & 31));
+            }
+        }
+        __syncwarp();
+        Set<W> keep;
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            keep.w[i] = scratch[threadIdx.x][2 * i] | (static_cast<u64>(scratch[threadIdx.x][2 * i + 1]) << 32);
+        return valid ? keep : Set<W>::zero();
+    }
 }
 
 template <int W>

@@ -171,6 +171,7 @@ template <int W, bool MMW, bool BLOOM>
 __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __restrict__ P, Control* C,
                                                             Bufs B) {
     __shared__ Set<W> adj[64 * W];
+    __shared__ unsigned mmw_keep[MMW ? kThreads : 1][2 * W];
     if (halted(C)) return;
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
         const u64 idx = base + lane;
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        const Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned) : Set<W>::zero();
+        const Set<W> M = warp_candidates<W, MMW>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         offered += M.count();
         winners += M.count();
         if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bloom_dedup(const Params* __res
     extern __shared__ __align__(16) u64 local_slots[];
     __shared__ Set<W> adj[64 * W];
     __shared__ unsigned novel_words[kThreads][2 * W];
+    __shared__ unsigned mmw_keep[MMW ? kThreads : 1][2 * W];
     if (halted(C)) return;
     const unsigned r = C->round;
     const unsigned epoch = C->epoch;
@@ -456,8 +458,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bloom_dedup(const Params* __res
         const u64 idx = base + lane;
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        const Set<W> M = valid ? candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned)
-                               : Set<W>::zero();
+        const Set<W> M = warp_candidates<W, MMW>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         offered += M.count();
         for (unsigned i = lane; i < kWarpSlots * W; i += 32) my_slots[i] = 0;
 #pragma unroll
