@@ -109,6 +109,11 @@ ELIMTW_API void etwg_shard_info(int* world, int* rank, int* is_virtual);
  * (CUDA IPC; ETWG_EXCHANGE=nccl or a failed peer mapping selects NCCL
  * grouped send/recv instead) */
 ELIMTW_API int etwg_shard_exchange_p2p(void);
+/* Layers of up to `states` states are expanded redundantly by every shard on
+ * the single-device engine (no routing: cheaper than an exchange for small
+ * layers); the first larger layer is split by owner and the decide continues
+ * sharded. Default 2^21 (env ETWG_HANDOFF); 0 shards from the root. */
+ELIMTW_API void etwg_set_shard_handoff(uint64_t states);
 
 /* host preprocessing (no GPU needed); rows as above */
 ELIMTW_API void etwg_graph_rows(const etw_graph* g, uint64_t* rows);

@@ -472,6 +472,13 @@ void etwg_shard_release(void) {
     }
 }
 
+void etwg_set_shard_handoff(uint64_t states) {
+    try {
+        shard_set_handoff(states);
+    } catch (...) {
+    }
+}
+
 int etwg_shard_exchange_p2p(void) {
     try {
         return shard_p2p();

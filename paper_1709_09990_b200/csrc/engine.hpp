@@ -69,6 +69,24 @@ using LayerObserver = std::function<void(int k, int round, const std::vector<Sta
 DecideResult device_decide(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg,
                            int rounds = -1, const LayerObserver* observer = nullptr);
 
+// Replicated prefix of an owner-sharded decide: the single-device engine runs
+// the decide until a layer exceeds `handoff_above` states (small layers are
+// cheaper to expand redundantly on every GPU than to route). When it stops
+// there, `handed` is set and the layer (device pointers, valid until the
+// engine's next call) is left for the shards; the result holds the rounds run.
+struct EngineLayer {
+    const void* keys = nullptr;      // u64[W] per state
+    const unsigned* hist = nullptr;  // u32 per state
+    uint64_t count = 0;
+    int W = 1;
+    int rounds_done = 0;
+    bool handed = false;
+};
+DecideResult device_decide_prefix(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg,
+                                  int rounds, const LayerObserver* observer, uint64_t handoff_above,
+                                  EngineLayer& handoff);
+int engine_device();  // the single-device engine's CUDA device (-1 without one)
+
 struct ExpandResult {
     std::vector<State> states;
     bool overflowed = false;
@@ -131,6 +149,8 @@ void shard_init_nccl(const unsigned char* id128, int rank, int world, int device
 void shard_release();
 void shard_info(int* world, int* rank, int* virt);
 int shard_p2p();  // 1 when the NCCL path pulls records over NVLink (CUDA IPC)
+// layers up to `states` run replicated on the single-device engine (0: shard from the root)
+void shard_set_handoff(uint64_t states);
 void shard_timer_begin();
 double shard_timer_end();
 void shard_accumulate(KernelTimes& t);

@@ -460,6 +460,67 @@ __global__ void __launch_bounds__(kRouteThreads) k_owner_compact(ShardCtl* C, Sh
 }
 
 // ----------------------------------------------------------------------
+// Handoff from the replicated prefix: every rank holds the whole layer (in
+// rank order); each keeps the states it owns, in the same order.
+
+template <int W>
+__global__ void k_owner_histogram(const u64* __restrict__ keys, u64 E, int G, unsigned long long* counts) {
+    __shared__ unsigned local[kMaxShards];
+    if (threadIdx.x < kMaxShards) local[threadIdx.x] = 0;
+    __syncthreads();
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < E; i += stride)
+        atomicAdd(&local[owner_of<W>(load_set<W>(keys, i), G)], 1u);
+    __syncthreads();
+    if (threadIdx.x < G && local[threadIdx.x]) atomicAdd(counts + threadIdx.x, static_cast<unsigned long long>(local[threadIdx.x]));
+}
+
+// tiles of 2048 states by ticket: block scan of the owned flags, decoupled
+// look-back over tiles, ordered stores
+template <int W>
+__global__ void __launch_bounds__(kRouteThreads) k_take_owned(const u64* __restrict__ keys,
+                                                              const unsigned* __restrict__ hist, u64 E, int G,
+                                                              int me, u64* out, unsigned* hout, u64* tiles,
+                                                              unsigned epoch, unsigned long long* ticket) {
+    using BlockScan = cub::BlockScan<unsigned, kRouteThreads>;
+    constexpr int ITEMS = 8;
+    constexpr u64 kSpan = static_cast<u64>(kRouteThreads) * ITEMS;
+    __shared__ typename BlockScan::TempStorage scan_tmp;
+    __shared__ u64 s_prefix, s_tile;
+    const u64 ntiles = (E + kSpan - 1) / kSpan;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1ull);
+        __syncthreads();
+        const u64 tile = s_tile;
+        if (tile >= ntiles) break;
+        // thread t holds states tile*span + t*ITEMS + i: its run is contiguous
+        Set<W> S[ITEMS];
+        unsigned H[ITEMS], mine = 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const u64 idx = tile * kSpan + static_cast<u64>(threadIdx.x) * ITEMS + i;
+            const bool valid = idx < E;
+            S[i] = valid ? load_set<W>(keys, idx) : Set<W>::zero();
+            H[i] = valid ? hist[idx] : 0u;
+            if (valid && static_cast<int>(owner_of<W>(S[i], G)) == me) mine |= 1u << i;
+        }
+        unsigned excl, total;
+        BlockScan(scan_tmp).ExclusiveSum(static_cast<unsigned>(__popc(mine)), excl, total);
+        if (threadIdx.x == 0) s_prefix = look_back(tiles, tile, total, epoch);
+        __syncthreads();
+        u64 pos = s_prefix + excl;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            if (!(mine >> i & 1u)) continue;
+            store_set<W>(out, pos, S[i]);
+            hout[pos] = H[i];
+            ++pos;
+        }
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------------
 // k_finish: global counters (all[] holds every shard's ShardStat)
 
 __global__ void k_shard_finish(const Params* __restrict__ P, ShardCtl* C, Plan pl) {
@@ -626,6 +687,9 @@ public:
         rank_ = 0;
     }
 
+    void set_handoff(u64 states) { handoff_ = states; }
+    u64 handoff() const { return handoff_; }
+
     // exchange mode of the NCCL path: 1 = owners read peers' outboxes over
     // NVLink (CUDA IPC), 0 = NCCL grouped send/recv of the outbox blocks
     int p2p() const { return p2p_ ? 1 : 0; }
@@ -676,15 +740,43 @@ public:
             return res;
         }
         check(cudaEventRecord(ev_[0], stream_), "event");
-        for (Shard& s : local_) setup(s, g, k, forbidden, cfg, rounds);
         np_floor_ = 1;
         cap_floor_ = 0;
         const bool bloom = cfg.dedup == DedupMode::bloom;
         // host mirror of the global round state
         std::vector<u64> count(G_, 0);
-        count[0] = 1;  // the root (empty set, history 0xFFFFFFFF) starts on shard 0
         ShardRound prev{};
         int r = 0;
+        if (handoff_ > 0) {
+            // replicated prefix: small layers run on the single-device engine on
+            // every rank (identical results, no communication)
+            if (engine_device() != device_)
+                throw DeviceError("the single-device engine and the shard run on different devices "
+                                  "(set ETWG_DEVICE to the shard's device before the first call)");
+            EngineLayer lay;
+            DecideResult pre = device_decide_prefix(g, k, forbidden, cfg, rounds, observer, handoff_, lay);
+            if (!lay.handed) {
+                check(cudaEventRecord(ev_[1], stream_), "event");
+                check(cudaEventSynchronize(ev_[1]), "event sync");
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
+                decide_ms_ += ms;
+                return pre;
+            }
+            r = lay.rounds_done;
+            res.rounds = pre.rounds;
+            const LayerStats& last = pre.rounds.back();
+            prev.expanded = last.expanded;
+            prev.unique = last.emitted;
+            prev.routed = last.emitted + last.duplicates;
+            prev.emitted = last.emitted;
+            count = owner_counts(lay);
+            for (Shard& s : local_) setup(s, g, k, forbidden, cfg, rounds, r, &lay, count[s.me]);
+        } else {
+            for (Shard& s : local_) setup(s, g, k, forbidden, cfg, rounds);
+            count[0] = 1;  // the root (empty set, history 0xFFFFFFFF) starts on shard 0
+        }
+        const int r_first = r;
         bool stopped = false;
         while (r < rounds && !stopped) {
             const Plan pl = plan(r, count, prev, cfg, W);
@@ -766,7 +858,8 @@ public:
         }
         const ShardCtl& c0 = *local_[0].h_ctl;
         bool any_ovf = false;
-        for (int i = 0; i < rounds; ++i) {
+        for (const LayerStats& ls : res.rounds) any_ovf = any_ovf || ls.overflowed;
+        for (int i = r_first; i < rounds; ++i) {
             const ShardRound& s = c0.rs[i];
             if (!s.valid) break;
             LayerStats ls;
@@ -785,7 +878,7 @@ public:
         // SURVEY §8d algorithmic bytes (same model as the single-device engine)
         // plus the records that crossed to other shards
         const double wb = 8.0 * W + 4.0, db = cfg.dedup == DedupMode::bloom ? 4.0 * cfg.bloom_hashes : 8.0 * W + 8.0;
-        for (int i = 0; i < rounds && c0.rs[i].valid; ++i) {
+        for (int i = r_first; i < rounds && c0.rs[i].valid; ++i) {
             const ShardRound& s = c0.rs[i];
             layer_bytes_ += wb * static_cast<double>(s.expanded + s.emitted);
             dedup_bytes_ += db * static_cast<double>(s.offered);
@@ -830,6 +923,14 @@ private:
     bool trace_ = std::getenv("ETWG_SHARD_TRACE") != nullptr;
     u64* d_wit_ = nullptr;
     int pl_round_parity_ = 0;  // buffer holding the current round's input layer
+    u64* d_scratch_ = nullptr;  // histogram counters + handoff ticket
+    // layers up to this many states are expanded redundantly by every shard
+    // on the single-device engine (no routing); the first larger layer is
+    // split by owner. ETWG_HANDOFF=0 shards from the root.
+    u64 handoff_ = [] {
+        const char* e = std::getenv("ETWG_HANDOFF");
+        return e ? std::strtoull(e, nullptr, 10) : (u64{1} << 21);
+    }();
     bool p2p_ = false;          // NCCL mode: pull records over NVLink instead of send/recv
     bool handles_dirty_ = false;  // outboxes (re)allocated since the last handle exchange
     const u64* peer_out_[kMaxShards] = {};
@@ -922,7 +1023,11 @@ private:
         s = Shard{};
     }
 
-    void setup(Shard& s, const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg, int rounds) {
+    // Params + control of shard s for a decide starting at round r0: the
+    // root on shard 0 (r0 = 0), or this shard's owned part of the engine's
+    // replicated layer (handoff).
+    void setup(Shard& s, const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg, int rounds,
+               int r0 = 0, const EngineLayer* from = nullptr, u64 owned = 0) {
         Params& p = *s.h_params;
         std::memset(&p, 0, sizeof p);
         p.n = g.vertex_count();
@@ -946,6 +1051,14 @@ private:
         const unsigned epoch = c.epoch;
         std::memset(&c, 0, sizeof c);
         c.epoch = next_epoch(s, epoch);
+        if (from) {
+            c.round = static_cast<unsigned>(r0);
+            c.count[r0 & 1] = owned;
+            grow_layers(s, owned + owned / 4 + 1024, 0, 0);
+            take_owned(s, *from, r0 & 1);
+            check(cudaMemcpyAsync(s.d_ctl, s.h_ctl, sizeof(ShardCtl), cudaMemcpyHostToDevice, stream_), "control");
+            return;
+        }
         c.count[0] = s.me == 0 ? 1 : 0;
         check(cudaMemcpyAsync(s.d_ctl, s.h_ctl, sizeof(ShardCtl), cudaMemcpyHostToDevice, stream_), "control");
         grow_layers(s, 1 << 16, 0, 0);
@@ -956,6 +1069,52 @@ private:
             check(cudaMemcpyAsync(s.b.hist[0], &root_hist, 4, cudaMemcpyHostToDevice, stream_), "root");
             check(cudaStreamSynchronize(stream_), "root");
         }
+    }
+
+    // per-owner state counts of the engine's layer (identical on every rank)
+    std::vector<u64> owner_counts(const EngineLayer& L) {
+        if (!d_scratch_) check(cudaMalloc(&d_scratch_, 256), "scratch");
+        check(cudaMemsetAsync(d_scratch_, 0, 8 * kMaxShards, stream_), "scratch");
+        const int grid = static_cast<int>(std::min<u64>((L.count + 255) / 256, 4096));
+        if (L.W == 1)
+            k_owner_histogram<1><<<std::max(grid, 1), 256, 0, stream_>>>(static_cast<const u64*>(L.keys), L.count, G_,
+                                                                         reinterpret_cast<unsigned long long*>(d_scratch_));
+        else
+            k_owner_histogram<2><<<std::max(grid, 1), 256, 0, stream_>>>(static_cast<const u64*>(L.keys), L.count, G_,
+                                                                         reinterpret_cast<unsigned long long*>(d_scratch_));
+        check(cudaGetLastError(), "owner histogram");
+        ++launches_;
+        std::vector<u64> c(G_);
+        check(cudaMemcpyAsync(c.data(), d_scratch_, 8 * G_, cudaMemcpyDeviceToHost, stream_), "owner counts");
+        check(cudaStreamSynchronize(stream_), "owner counts");
+        return c;
+    }
+
+    // the engine's layer -> this shard's layer buffer `buf`, owned states only, in order
+    void take_owned(Shard& s, const EngineLayer& L, int buf) {
+        const u64 tiles_needed = (L.count + 2047) / 2048 + 1;
+        if (tiles_needed > s.b.tile_cap || !s.b.tiles) {
+            const u64 cap = std::max<u64>(tiles_needed * 2, u64{1} << 12);
+            cudaFree(s.b.tiles);
+            check(cudaMalloc(&s.b.tiles, cap * 8), "tiles");
+            check(cudaMemsetAsync(s.b.tiles, 0, cap * 8, stream_), "tiles");
+            s.b.tile_cap = cap;
+        }
+        s.h_ctl->epoch = next_epoch(s, s.h_ctl->epoch);
+        const unsigned epoch = s.h_ctl->epoch;
+        s.h_ctl->epoch = next_epoch(s, epoch);  // the first sharded round gets a fresh epoch
+        if (!d_scratch_) check(cudaMalloc(&d_scratch_, 256), "scratch");
+        unsigned long long* ticket = reinterpret_cast<unsigned long long*>(d_scratch_) + kMaxShards;
+        check(cudaMemsetAsync(ticket, 0, 8, stream_), "ticket");
+        const int grid = std::max(1, std::min(grid_route_[0], static_cast<int>((L.count + 2047) / 2048)));
+        if (L.W == 1)
+            k_take_owned<1><<<grid, kRouteThreads, 0, stream_>>>(static_cast<const u64*>(L.keys), L.hist, L.count, G_,
+                                                                 s.me, s.b.keys[buf], s.b.hist[buf], s.b.tiles, epoch, ticket);
+        else
+            k_take_owned<2><<<grid, kRouteThreads, 0, stream_>>>(static_cast<const u64*>(L.keys), L.hist, L.count, G_,
+                                                                 s.me, s.b.keys[buf], s.b.hist[buf], s.b.tiles, epoch, ticket);
+        check(cudaGetLastError(), "take owned");
+        ++launches_;
     }
 
     unsigned next_epoch(Shard& s, unsigned e) {
@@ -1378,6 +1537,12 @@ void shard_info(int* world, int* rank, int* virt) {
     ShardSet& s = ShardSet::instance();
     std::lock_guard<std::mutex> lock(s.mu);
     s.info(world, rank, virt);
+}
+
+void shard_set_handoff(uint64_t states) {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.set_handoff(states);
 }
 
 int shard_p2p() {

@@ -75,6 +75,8 @@ struct Control {
     unsigned epoch;     // look-back tag of the current round attempt (never 0)
     unsigned exits;     // CTAs that finished the round's last pass
     unsigned pad;
+    u64 handoff_above;  // >0: stop (handed = 1) once a layer exceeds this many states
+    unsigned handed, pad2;
     u64 part_floor;     // exact mode: minimum partitions after a grow (per decide)
     u64 rec_floor;      // exact mode: minimum records per partition after a grow
     RoundStats rs[kMaxRounds];
@@ -573,7 +575,12 @@ __device__ __forceinline__ void finish_round(const Params* P, Control* C, const 
     C->count[(r + 1) & 1] = emitted;
     C->round = r + 1;
     C->epoch = (C->epoch & kEpochMask) == kEpochMask ? 1 : C->epoch + 1;
-    if (emitted == 0 || static_cast<int>(r) + 1 >= P->rounds) C->stop = 1;
+    if (emitted == 0 || static_cast<int>(r) + 1 >= P->rounds) {
+        C->stop = 1;
+    } else if (C->handoff_above && emitted > C->handoff_above) {
+        C->stop = 1;  // the owner-sharded engine takes the layer from here
+        C->handed = 1;
+    }
 }
 
 // A tile is ITEMS slices of kThreads consecutive parents (slice i = parents
@@ -686,7 +693,8 @@ public:
     }
 
     DecideResult decide(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg,
-                        int rounds, const LayerObserver* observer) {
+                        int rounds, const LayerObserver* observer, u64 handoff_above = 0,
+                        EngineLayer* handoff = nullptr) {
         require_device();
         const int n = g.vertex_count();
         const int W = n > 64 ? 2 : 1;
@@ -700,7 +708,7 @@ public:
         setup_params(g, k, forbidden, cfg, rounds, /*any_pop=*/0);
         // root layer: {(empty set, 0xFFFFFFFF)}
         ensure_layers(1, 0, 0);
-        reset_control(1);
+        reset_control(1, handoff_above);
         u64 zero2[2] = {0, 0};
         unsigned root_hist = 0xFFFFFFFFu;
         copy(b_.keys[0], zero2, 16, cudaMemcpyHostToDevice, "root");
@@ -727,6 +735,18 @@ public:
         }
         res.overflowed = any_ovf;
         account(res.rounds, W, cfg);
+        if (h_ctl_->handed) {
+            if (!handoff) throw DeviceError("device decide handed off without a receiver");
+            const int done = static_cast<int>(res.rounds.size());
+            handoff->keys = b_.keys[done & 1];
+            handoff->hist = b_.hist[done & 1];
+            handoff->count = h_ctl_->count[done & 1];
+            handoff->W = W;
+            handoff->rounds_done = done;
+            handoff->handed = true;
+            return res;
+        }
+        if (handoff) handoff->handed = false;
         const bool empty = !res.rounds.empty() && res.rounds.back().emitted == 0;
         if (empty) {
             res.outcome = any_ovf ? Outcome::indeterminate : Outcome::infeasible;
@@ -959,10 +979,11 @@ private:
         copy(d_params_, h_params_, sizeof(Params), cudaMemcpyHostToDevice, "params");
     }
 
-    void reset_control(u64 first_count) {
+    void reset_control(u64 first_count, u64 handoff_above = 0) {
         Control& c = *h_ctl_;
         std::memset(&c, 0, sizeof c);
         c.count[0] = first_count;
+        c.handoff_above = handoff_above;
         c.epoch = next_epoch();
         copy(d_ctl_, h_ctl_, sizeof(Control), cudaMemcpyHostToDevice, "control");
     }
@@ -1312,6 +1333,23 @@ DecideResult device_decide(const Graph& g, int k, const HostSet& forbidden, cons
     Engine& e = Engine::instance();
     std::lock_guard<std::mutex> lock(e.mu);
     return e.decide(g, k, forbidden, cfg, rounds, observer);
+}
+
+DecideResult device_decide_prefix(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg,
+                                  int rounds, const LayerObserver* observer, uint64_t handoff_above,
+                                  EngineLayer& handoff) {
+    if (k < 0) throw std::invalid_argument("k must be non-negative");
+    if (cfg.max_layer_states == 0) throw std::invalid_argument("layer capacity must be positive");
+    Engine& e = Engine::instance();
+    std::lock_guard<std::mutex> lock(e.mu);
+    handoff.handed = false;
+    return e.decide(g, k, forbidden, cfg, rounds, observer, handoff_above, &handoff);
+}
+
+int engine_device() {
+    Engine& e = Engine::instance();
+    std::lock_guard<std::mutex> lock(e.mu);
+    return e.ready() ? e.info().device : -1;
 }
 
 ExpandResult device_expand_layer(const Graph& g, int k, const HostSet& forbidden,

@@ -123,6 +123,7 @@ def library() -> C.CDLL:
         "etwg_shard_release": (None, []),
         "etwg_shard_info": (None, [_ip, _ip, _ip]),
         "etwg_shard_exchange_p2p": (C.c_int, []),
+        "etwg_set_shard_handoff": (None, [C.c_uint64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -480,6 +481,11 @@ def shard_init(uid: bytes, rank: int, world: int, device: int) -> None:
     st = library().etwg_shard_init(buf, rank, world, device, err, 1024)
     if st != ETW_OK:
         _raise(st, err)
+
+
+def set_shard_handoff(states: int) -> None:
+    """Layers up to `states` run replicated on every shard (0: shard from the root)."""
+    library().etwg_set_shard_handoff(states)
 
 
 def shard_release() -> None:

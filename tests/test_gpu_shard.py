@@ -18,11 +18,15 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture
 def shards(E, gpu):
-    def use(g):
+    """G virtual shards; by default sharded from the root (no replicated
+    prefix) so every round exercises route / owner."""
+    def use(g, handoff=0):
         E.set_virtual_shards(g)
+        E.set_shard_handoff(handoff)
         return g
     yield use
     E.set_virtual_shards(1)
+    E.set_shard_handoff(1 << 21)
 
 
 def _sets(run):
@@ -56,13 +60,15 @@ def _rows(name, rows):
     return elimtw.Graph.parse(instance_text(name)).rows()
 
 
-@pytest.mark.parametrize("g", [2, 3, 8])
-def test_sharded_exact_matches_single_device(E, shards, g):
+@pytest.mark.parametrize("g,handoff", [(2, 0), (3, 0), (8, 0), (3, 2000), (8, 50000)])
+def test_sharded_exact_matches_single_device(E, shards, g, handoff):
+    """handoff > 0: the first layers run replicated on the single-device
+    engine, the first layer above `handoff` states is split by owner."""
     base = {}
     for name, rows, k in CASES:
         rows = _rows(name, rows)
         base[(name, k)] = E.decide(rows, k, dedup="exact")
-    shards(g)
+    shards(g, handoff)
     for name, rows, k in CASES:
         rows = _rows(name, rows)
         got = E.decide(rows, k, dedup="exact")
@@ -146,13 +152,14 @@ def test_sharded_128bit_path(E, oracle, shards):
         assert _sets(a) == _sets(b)
 
 
-def test_sharded_solve_stats_identical(E, shards):
+@pytest.mark.parametrize("handoff", [0, 20000])
+def test_sharded_solve_stats_identical(E, shards, handoff):
     """etw_solve through the unchanged C API: the stats JSON (every layer
     counter of every attempt) equals the single-device solve's in exact mode,
     and the reconstructed order validates to the treewidth."""
     g = E.Graph.from_rows(G.random_graph(1, 40, 0.3))
     want = E.solve(g, E.Options(dedup="exact"))
-    shards(8)
+    shards(8, handoff)
     got = E.solve(g, E.Options(dedup="exact"))
     assert got.value == want.value == 22
     assert json.loads(got.stats_json) == json.loads(want.stats_json)
@@ -183,6 +190,7 @@ def test_nccl_one_rank_communicator(E, gpu):
     rows = G.random_graph(1, 40, 0.3)
     want = {k: E.decide(rows, k, dedup="exact") for k in (21, 22)}
     E.shard_init(E.nccl_unique_id(), 0, 1, gpu["device"])
+    E.set_shard_handoff(3000)  # replicated prefix, then the NCCL-path rounds
     try:
         assert E.shard_info() == {"world": 1, "rank": 0, "virtual": False, "p2p": False}
         for k, w in want.items():
@@ -195,3 +203,4 @@ def test_nccl_one_rank_communicator(E, gpu):
         assert res.value == 22
     finally:
         E.shard_release()
+        E.set_shard_handoff(1 << 21)
