@@ -245,8 +245,24 @@ def roofline(p):
     achieved = bytes_ / (ms / 1e3) / 1e9 if ms > 0 else 0.0
     total_ms = sum(v[0] for v in classes.values())
     round_bytes = sum(v[2] for v in classes.values())
+    # DRAM traffic from the committed ncu --set full capture of this kernel's
+    # longest launch (tools/ncu_traffic.py), scaled to the average launch
+    traffic, traffic_src, alu = None, None, None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr = json.load(f).get(name)
+        if tr:
+            traffic = tr["traffic_over_algorithmic"] * per_launch
+            traffic_src = (f"profiles/r01_traffic.json: ncu --set full of the longest launch, DRAM bytes = "
+                           f"{tr['traffic_over_algorithmic']:.2f} x algorithmic bytes, scaled to the average launch")
+            if "issue_slots_busy_pct" in tr:
+                alu = {"bound": "integer ALU issue", "issue_slots_busy_pct": tr["issue_slots_busy_pct"],
+                       "ipc": tr["ipc"], "sm_throughput_pct": tr["sm_throughput_pct"],
+                       "source": "same capture"}
     return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "compute_view": alu, "peak_source": peak_src,
             "avg_launch_us": 1e3 * avg_ms, "launches": int(n),
             "algorithmic_bytes_per_launch": per_launch,
             "share_of_wavefront_time": ms / total_ms if total_ms else None,

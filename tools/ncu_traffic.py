@@ -38,7 +38,10 @@ def metrics(rep):
                  "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}.get(u.get(k, ""), 1)
         return x * scale
     return {"dram_bytes": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
-            "duration_s": val("gpu__time_duration.sum")}
+            "duration_s": val("gpu__time_duration.sum"),
+            "ipc": val("sm__inst_executed.avg.per_cycle_active"),
+            "issue_pct": val("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
+            "sm_pct": val("sm__throughput.avg.pct_of_peak_sustained_elapsed")}
 
 
 res = {"round": {"index": r, "expanded": E, "emitted": U, "offered": P}}
@@ -52,6 +55,7 @@ for arg in sys.argv[3:]:
     a = alg[name] / shards
     res[name] = {"traffic_bytes": m["dram_bytes"], "algorithmic_bytes": a,
                  "traffic_over_algorithmic": m["dram_bytes"] / a, "duration_ms": 1e3 * m["duration_s"],
-                 "algorithmic_GBps": a / m["duration_s"] / 1e9, "dram_GBps": m["dram_bytes"] / m["duration_s"] / 1e9}
+                 "algorithmic_GBps": a / m["duration_s"] / 1e9, "dram_GBps": m["dram_bytes"] / m["duration_s"] / 1e9,
+                 "ipc": m["ipc"], "issue_slots_busy_pct": m["issue_pct"], "sm_throughput_pct": m["sm_pct"]}
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps(res, indent=1))
