@@ -908,6 +908,10 @@ private:
         };
         allow_exact(k_exact_scatter<1, false, false>, 0, grid_exact_[0]);
         allow_exact(k_exact_scatter<2, false, false>, 0, grid_exact_[1]);
+        if (const char* c = std::getenv("ETWG_SCATTER_CTAS")) {  // CTAs per SM (tuning sweeps)
+            const int per = std::atoi(c);
+            for (int w = 0; w < 2; ++w) grid_exact_[w] = std::min(grid_exact_[w], prop.multiProcessorCount * per);
+        }
         allow_exact(k_exact_scatter<1, true, false>, 0, grid_exact_mmw_[0]);
         allow_exact(k_exact_scatter<2, true, false>, 0, grid_exact_mmw_[1]);
         {

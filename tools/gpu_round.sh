@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 300 python bench.py --impl reference --steps 2 --warmup 1 2>&1 | tail -1 | cut -c1-400
+for c in 2 3 4 5 6; do echo "ctas $c"; ETWG_SCATTER_CTAS=$c timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | sed -n 2p; done
