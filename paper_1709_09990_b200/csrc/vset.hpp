@@ -171,4 +171,45 @@ ETW_HD Members<W> members(const Set<W>& s) {
     return Members<W>{s};
 }
 
+// Removes and returns some member (the highest) of a non-empty set. Where
+// the visiting order does not matter this is the cheap pop on the device:
+// one FLO per 32-bit word instead of the 64-bit ffs + borrow of pop().
+template <int W>
+ETW_HD int pop_any(Set<W>& s) {
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+    for (int i = W - 1; i >= 0; --i) {
+        const unsigned hi = static_cast<unsigned>(s.w[i] >> 32);
+        const unsigned lo = static_cast<unsigned>(s.w[i]);
+        if (hi | lo) {
+            const int b = hi ? 63 - __clz(hi) : 31 - __clz(lo);
+            s.w[i] ^= uint64_t{1} << b;
+            return 64 * i + b;
+        }
+    }
+    return -1;
+#else
+    return s.pop();
+#endif
+}
+
+// Calls f(v) for every member, in no particular order (descending on the
+// device, 32-bit words, one FLO + one XOR per member).
+template <int W, typename F>
+ETW_HD void for_each_any(const Set<W>& s, F&& f) {
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+    for (int i = 2 * W - 1; i >= 0; --i) {
+        unsigned x = static_cast<unsigned>(s.w[i >> 1] >> (32 * (i & 1)));
+        while (x) {
+            const int b = 31 - __clz(x);
+            x ^= 1u << b;
+            f(32 * i + b);
+        }
+    }
+#else
+    for (int v : members(s)) f(v);
+#endif
+}
+
 }  // namespace etw

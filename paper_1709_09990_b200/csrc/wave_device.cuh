@@ -220,11 +220,12 @@ template <int W, bool COMPACT>
 __device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>& S, Set<W>* R) {
     Set<W> rem = S;
     while (rem.any()) {
-        Set<W> comp = Set<W>::bit(rem.lowest());
-        Set<W> frontier = comp;
+        Set<W> frontier = rem;
+        Set<W> comp = Set<W>::bit(pop_any(frontier));  // any seed
+        frontier = comp;
         Set<W> nb = Set<W>::zero();
         while (frontier.any()) {
-            const Set<W> a = adj[frontier.pop()];
+            const Set<W> a = adj[pop_any(frontier)];
             nb |= a;
             Set<W> fresh = (a & S) - comp;
             comp |= fresh;
@@ -233,7 +234,7 @@ __device__ __forceinline__ void component_reach(const Set<W>* adj, const Set<W>&
         rem = rem - comp;
         const Set<W> boundary = nb - S;
         if (boundary.none()) continue;
-        for (int u : members(comp)) R[reach_slot<W, COMPACT>(S, u)] = boundary;
+        for_each_any(comp, [&](int u) { R[reach_slot<W, COMPACT>(S, u)] = boundary; });
     }
 }
 
@@ -244,7 +245,7 @@ template <int W, bool COMPACT>
 __device__ __forceinline__ Set<W> reach_from(const Set<W>* adj, const Set<W>& S, const Set<W>* R,
                                              int v) {
     Set<W> q = adj[v] - S;
-    for (int u : members(adj[v] & S)) q |= R[reach_slot<W, COMPACT>(S, u)];
+    for_each_any(adj[v] & S, [&](int u) { q |= R[reach_slot<W, COMPACT>(S, u)]; });
     q.del(v);
     return q;
 }
@@ -331,10 +332,10 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
     Set<W> R[N];
     component_reach<W, COMPACT>(adj, S, R);
     if constexpr (!MMW) {
-        for (int v : members(eligible)) {
-            if ((adj[v] - S).count() > k) continue;  // |Q(S,v)| >= |N(v) \ S|
+        for_each_any(eligible, [&](int v) {
+            if ((adj[v] - S).count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
             if (reach_from<W, COMPACT>(adj, S, R, v).count() <= k) keep.add(v);
-        }
+        });
     } else {
         Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
         for (int w : members(open)) rows[w] = reach_from<W, COMPACT>(adj, S, R, w);

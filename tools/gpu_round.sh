@@ -1,2 +1,5 @@
 mkdir -p gpurun_out
-for c in 2 3 4 5 6; do echo "ctas $c"; ETWG_SCATTER_CTAS=$c timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | sed -n 2p; done
+timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 2>&1 | tail -1
+timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | sed -n 2p
+VSHARDS=2 ETWG_HANDOFF=0 timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | sed -n 2p
+timeout 600 python tools/prof_g48.py exact 2>&1 | head -5
