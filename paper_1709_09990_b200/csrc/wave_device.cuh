@@ -407,19 +407,7 @@ __device__ __forceinline__ void load_adjacency(const Params* P, Set<W>* adj) {
 }
 
 // ----------------------------------------------------------------------
-// K2a: exact dedup — open addressing, claim by CAS, keep min emission rank
-// (replaces the exact branch's sort/unique, dp.cpp:118-151)
-
-// Rank words carry a round tag in bits 48..63 that shrinks as rounds
-// advance, so any stale rank left by an earlier round of this decide loses
-// every atomicMin; keys of a round all have popcount round+1, so stale keys
-// are recognised without clearing the table between rounds.
-__device__ __forceinline__ u64 rank_tag(unsigned r) { return static_cast<u64>(kMaxRounds - r) << 48; }
-
-template <int W>
-__device__ __forceinline__ bool stale_key(const Set<W>& cur, int want_pop) {
-    return want_pop < 0 ? cur.none() : cur.count() != want_pop;
-}
+// 128-bit global compare-and-swap (atom.global.cas.b128, sm_90+)
 
 __device__ __forceinline__ void cas128(u64* addr, u64 exp_lo, u64 exp_hi, u64 new_lo, u64 new_hi,
                                        u64& old_lo, u64& old_hi) {
@@ -432,88 +420,6 @@ __device__ __forceinline__ void cas128(u64* addr, u64 exp_lo, u64 exp_hi, u64 ne
         : "=l"(old_lo), "=l"(old_hi)
         : "l"(exp_lo), "l"(exp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
         : "memory");
-}
-
-// Slot layout: W=1 {key, rank}; W=2 {key.lo, key.hi, rank, pad}.
-template <int W>
-__device__ __forceinline__ u64* table_slot(u64* table, u64 i) {
-    return table + i * (W == 1 ? 2 : 4);
-}
-
-// Inserts `key` with `rank` (kept as the minimum of all inserts of the key).
-// Returns 1 when this call claimed a fresh slot for the key, 0 when the key
-// was present, -1 when `max_probes` slots were probed without finding a
-// place (the table is over-full: the caller aborts the round and grows it).
-constexpr int kMaxProbes = 1 << 12;
-
-template <int W>
-__device__ int table_insert(u64* table, u64 mask, int want_pop, const Set<W>& key, u64 rank,
-                            int max_probes = kMaxProbes) {
-    u64 i = slot_hash<W>(key) & mask;
-    for (int probe = 0; probe < max_probes; ++probe) {
-        u64* slot = table_slot<W>(table, i);
-        int fresh = 0;
-        if constexpr (W == 1) {
-            u64 cur = *reinterpret_cast<volatile u64*>(slot);
-            for (;;) {
-                if (cur == key.w[0]) break;
-                Set<1> c;
-                c.w[0] = cur;
-                if (!stale_key<1>(c, want_pop)) break;
-                u64 prev = atomicCAS(slot, cur, key.w[0]);
-                if (prev == cur) {
-                    cur = key.w[0];
-                    fresh = 1;
-                    break;
-                }
-                cur = prev;
-            }
-            if (cur == key.w[0]) {
-                atomicMin(slot + 1, rank);
-                return fresh;
-            }
-        } else {
-            // 128-bit keys: read through a failing CAS so the view is never torn
-            u64 lo, hi;
-            cas128(slot, ~u64{0}, ~u64{0}, ~u64{0}, ~u64{0}, lo, hi);
-            for (;;) {
-                if (lo == key.w[0] && hi == key.w[1]) break;
-                Set<2> c;
-                c.w[0] = lo;
-                c.w[1] = hi;
-                if (!stale_key<2>(c, want_pop)) break;
-                u64 plo, phi;
-                cas128(slot, lo, hi, key.w[0], key.w[1], plo, phi);
-                if (plo == lo && phi == hi) {
-                    lo = key.w[0];
-                    hi = key.w[1];
-                    fresh = 1;
-                    break;
-                }
-                lo = plo;
-                hi = phi;
-            }
-            if (lo == key.w[0] && hi == key.w[1]) {
-                atomicMin(slot + 2, rank);
-                return fresh;
-            }
-        }
-        i = (i + 1) & mask;
-    }
-    return -1;
-}
-
-// After all inserts of the round: the rank stored with `key`.
-template <int W>
-__device__ __forceinline__ u64 table_rank(const u64* table, u64 mask, const Set<W>& key) {
-    u64 i = slot_hash<W>(key) & mask;
-    for (;;) {
-        const u64* slot = table + i * (W == 1 ? 2 : 4);
-        bool hit = slot[0] == key.w[0];
-        if constexpr (W == 2) hit = hit && slot[1] == key.w[1];
-        if (hit) return slot[W == 1 ? 1 : 2];
-        i = (i + 1) & mask;
-    }
 }
 
 template <int W>
@@ -542,19 +448,6 @@ __device__ __forceinline__ bool smem_claim(u64* keys, unsigned h, const Set<W>& 
             : "memory");
         return (lo | hi) == 0 || (lo == key.w[0] && hi == key.w[1]);
     }
-}
-
-// Shared-memory lookup after all claims: slot of `key` or -1.
-template <int W>
-__device__ __forceinline__ int smem_find(const u64* keys, unsigned h, unsigned mask, const Set<W>& key,
-                                         int max_probes) {
-    for (int probe = 0; probe < max_probes; ++probe) {
-        bool hit = keys[W * h] == key.w[0];
-        if constexpr (W == 2) hit = hit && keys[2 * h + 1] == key.w[1];
-        if (hit) return static_cast<int>(h);
-        h = (h + 1) & mask;
-    }
-    return -1;
 }
 
 // ----------------------------------------------------------------------
