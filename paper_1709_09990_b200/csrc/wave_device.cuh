@@ -401,6 +401,60 @@ __device__ __forceinline__ Set<W> warp_candidates(const Set<W>* adj, int n, int 
     }
 }
 
+// Warp-per-parent candidate evaluation for small layers (call with all 32
+// lanes, S warp-uniform). With one thread per parent a round of a few
+// thousand states leaves the GPU idle and each thread walks ~n candidates
+// (and, with MMW, ~n minor contractions) serially; here lane 0 flood-fills
+// G[S] into the warp's shared boundary table R and the candidates (and
+// their MMW bounds) are spread over the lanes. R (and `rows`, for MMW) are
+// the warp's 64W-entry shared tables. Returns the warp-uniform keep mask;
+// `pruned` counts this lane's MMW prunes.
+template <int W, bool MMW>
+__device__ __forceinline__ Set<W> warp_parent_candidates(const Set<W>* adj, int n, int k, const Set<W>& S,
+                                                         const Set<W>& forbidden, u64& pruned, Set<W>* R,
+                                                         Set<W>* rows) {
+    const int lane = threadIdx.x & 31;
+    const Set<W> open = Set<W>::prefix(n) - S;
+    const Set<W> eligible = open - forbidden;
+    if (eligible.none()) return Set<W>::zero();
+    if (lane == 0) component_reach<W, false>(adj, S, R);
+    __syncwarp();
+    Set<W> mine = Set<W>::zero();
+    if constexpr (!MMW) {
+        const int ne = eligible.count();
+        for (int i = lane; i < ne; i += 32) {
+            const int v = nth_member<W>(eligible, i);
+            if ((adj[v] - S).count() > k) continue;
+            if (reach_from<W, false>(adj, S, R, v).count() <= k) mine.add(v);
+        }
+    } else {
+        const int no = open.count();
+        for (int i = lane; i < no; i += 32) {  // dp.cpp:51-53: Q(S,w) for every open w
+            const int w = nth_member<W>(open, i);
+            rows[w] = reach_from<W, false>(adj, S, R, w);
+        }
+        __syncwarp();
+        const int ne = eligible.count();
+        for (int i = lane; i < ne; i += 32) {
+            const int v = nth_member<W>(eligible, i);
+            if (rows[v].count() > k) continue;
+            if (mmw_child<W>(n, k, S, v, rows) > k)
+                ++pruned;
+            else
+                mine.add(v);
+        }
+    }
+    Set<W> keep;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        const unsigned lo = __reduce_or_sync(kFull, static_cast<unsigned>(mine.w[i]));
+        const unsigned hi = __reduce_or_sync(kFull, static_cast<unsigned>(mine.w[i] >> 32));
+        keep.w[i] = (static_cast<u64>(hi) << 32) | lo;
+    }
+    __syncwarp();  // R / rows are reused by the warp's next parent
+    return keep;
+}
+
 template <int W>
 __device__ __forceinline__ void load_adjacency(const Params* P, Set<W>* adj) {
     for (int i = threadIdx.x; i < P->n; i += blockDim.x) adj[i] = param_set<W>(P->rows[i]);

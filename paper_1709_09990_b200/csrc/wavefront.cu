@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
                                                             Bufs B) {
     __shared__ Set<W> adj[64 * W];
     __shared__ unsigned mmw_keep[MMW ? kThreads : 1][2 * W];
+    __shared__ Set<W> warp_tables[kThreads / 32][MMW ? 2 : 1][64 * W];  // small-layer mode
     if (halted(C)) return;
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
@@ -220,6 +221,46 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
     // parents are cheap never waits for the CTA's slowest warp
     const u64 nwarps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
     u64 offered = 0, pruned = 0, winners = 0;
+    // Small layer (fewer than 1/8 of the resident threads): one warp per
+    // parent, candidates and MMW bounds spread over the lanes.
+    if (E * 8 <= static_cast<u64>(gridDim.x) * blockDim.x) {
+        Set<W>* R = warp_tables[threadIdx.x >> 5][0];
+        Set<W>* rows = warp_tables[threadIdx.x >> 5][MMW ? 1 : 0];
+        bool full = false;
+        for (u64 p = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5; p < E; p += nwarps) {
+            if (*reinterpret_cast<volatile unsigned*>(&C->abort)) break;
+            const Set<W> S = load_set<W>(in, p);
+            const Set<W> M = warp_parent_candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned, R, rows);
+            const int cnt = M.count();
+            if (lane == 0) {
+                offered += cnt;
+                winners += cnt;
+                store_set<W>(B.cmask, p, Set<W>::zero());
+            }
+            for (int i = lane; i < cnt; i += 32) {
+                const int v = nth_member<W>(M, i);
+                Set<W> key = S;
+                key.add(v);
+                const u64 part = part_of<W>(key, pl.lg);
+                const unsigned slot = atomicAdd(B.cursors + part, 1u);
+                if (slot < pl.cap) {
+                    u64* rec = B.recs + (part * pl.cap + slot) * rec_words<W>();
+                    if constexpr (W == 1) {
+                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(p, v));
+                    } else {
+                        *reinterpret_cast<ulonglong4*>(rec) =
+                            make_ulonglong4(key.w[0], key.w[1], child_rank<W>(p, v), 0);
+                    }
+                } else {
+                    full = true;
+                }
+            }
+        }
+        if (__any_sync(kFull, full) && lane == 0) {
+            C->need = 2 * pl.cap;
+            C->abort = kGrowRecs;
+        }
+    } else
     for (u64 base = ((blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5) * 32; base < E;
          base += nwarps * 32) {
         if (*reinterpret_cast<volatile unsigned*>(&C->abort)) break;  // warp-uniform read
@@ -1170,8 +1211,10 @@ private:
         // take the partitioned path: exact per-bucket dedup in shared memory,
         // then the filter on each distinct key once (17 probes per distinct
         // child instead of per offered child)
+        // (and MMW decides: their small layers run the warp-per-parent scatter)
         part_bloom_ = bloom_round_ &&
-                      bloom_bits_for(cfg.max_layer_states, cfg.bloom_bits_per_element) > (u64{1} << 28) &&
+                      (bloom_bits_for(cfg.max_layer_states, cfg.bloom_bits_per_element) > (u64{1} << 28) ||
+                       cfg.use_mmw) &&
                       !(h_params_->flags & 64);
         if (bloom_round_) clean_blooms();
         if (!prof.on) check(cudaEventRecord(ev_[0], stream_), "event");
