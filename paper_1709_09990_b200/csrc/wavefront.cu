@@ -886,6 +886,10 @@ private:
     int grid_fused_ = 0;
     int grid_exact_[2] = {0, 0};
     int grid_exact_mmw_[2] = {0, 0};
+    int carveout_ = [] {
+        const char* e = std::getenv("ETWG_CARVEOUT");
+        return e ? std::atoi(e) : -1;  // -1: driver default
+    }();
     int grid_part_[2] = {0, 0};
     bool part_bloom_ = false;  // Bloom rounds of this decide use scatter/part/append
 
@@ -943,6 +947,10 @@ private:
         auto allow_exact = [&](auto kernel, int bytes, int& grid) {
             check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                   "smem attribute");
+            // K1's per-thread boundary tables live in local memory: keep the
+            // shared carve-out near what the resident CTAs need (ETWG_CARVEOUT %)
+            check(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_),
+                  "carveout");
             int blocks = 0;
             check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, bytes), "occupancy");
             grid = prop.multiProcessorCount * std::max(1, blocks);
