@@ -55,6 +55,9 @@ namespace etw {
 namespace {
 
 constexpr int kMaxShards = 8;
+#ifndef ETWG_ROUTE_COMPACT
+#define ETWG_ROUTE_COMPACT true  // rank-indexed boundary table for hash-ordered layers
+#endif
 constexpr int kOwnerThreads = 512;
 constexpr int kRouteThreads = 256;
 
@@ -106,6 +109,7 @@ struct Plan {
     u64 bloom_m;  // bits of the owner's Bloom slice (0: exact mode)
     u64 layer_est;  // host sizing hint: next-layer states per owner
     int lg, G, me, rounds;
+    int shared_r;   // k_route keeps K1's boundary tables in (dynamic) shared memory
 };
 
 struct ShardBufs {
@@ -185,7 +189,9 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
         const unsigned H = valid ? hin[idx] : 0u;
-        Set<W> M = warp_candidates<W, MMW, true>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
+        Set<W> M = warp_candidates<W, MMW, ETWG_ROUTE_COMPACT>(
+            adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep,
+            (!TILE && !MMW && W == 1 && pl.shared_r) ? reinterpret_cast<Set<W>*>(smem_raw) : nullptr);
         offered += M.count();
         if constexpr (TILE) {
             tile_set_clear<W, route_tile_slots<W>()>(ts);
@@ -919,6 +925,8 @@ private:
     uint64_t launches_ = 0, reruns_ = 0, expanded_ = 0, h2d_ = 0, d2h_ = 0, offered_ = 0, unique_ = 0;
     cudaEvent_t tev_[2] = {nullptr, nullptr};
     int grid_route_[2] = {0, 0}, grid_owner_[2] = {0, 0};
+    int grid_route_sh_ = 0;  // grid of the shared-boundary-table route variant
+    bool shared_r_ = true;
     bool tile_dedup_ = false;
     bool trace_ = std::getenv("ETWG_SHARD_TRACE") != nullptr;
     u64* d_wit_ = nullptr;
@@ -986,6 +994,11 @@ private:
         }
         grid_route_[0] = std::min(grid_route_[0], g_mmw[0]);
         grid_route_[1] = std::min(grid_route_[1], g_mmw[1]);
+        {
+            const char* e = std::getenv("ETWG_ROUTE_SHARED_R");
+            shared_r_ = !(e && e[0] == '0');
+            allow_route(k_route<1, false, false>, kShSlots * 8 * kRouteThreads, grid_route_sh_);
+        }
         if (const char* c = std::getenv("ETWG_ROUTE_CTAS")) {  // CTAs per SM (tuning sweeps)
             const int per = std::atoi(c);
             for (int w = 0; w < 2; ++w) grid_route_[w] = std::min(grid_route_[w], prop.multiProcessorCount * per);
@@ -1270,6 +1283,9 @@ private:
         if (tile_dedup_)
             k_route<W, MMW, true><<<grid_route_[W - 1], kRouteThreads, route_smem_bytes<W>(), stream_>>>(
                 s.d_params, s.d_ctl, s.b, p);
+        else if (W == 1 && !MMW && shared_r_)
+            k_route<W, MMW, false><<<grid_route_sh_, kRouteThreads, kShSlots * 8 * kRouteThreads, stream_>>>(
+                s.d_params, s.d_ctl, s.b, p);
         else
             k_route<W, MMW, false><<<grid_route_[W - 1], kRouteThreads, 0, stream_>>>(s.d_params, s.d_ctl, s.b, p);
     }
@@ -1277,6 +1293,7 @@ private:
     void launch_route(Shard& s, const Plan& pl, int W, bool mmw) {
         Plan p = pl;
         p.me = s.me;
+        p.shared_r = shared_r_ ? 1 : 0;
         if (W == 1) {
             if (mmw) route_kernel<1, true>(s, p);
             else route_kernel<1, false>(s, p);

@@ -321,14 +321,58 @@ __device__ int mmw_child(int n, int cap, const Set<W>& S, int v, const Set<W>* r
     return bound;
 }
 
+// Rank-indexed per-thread boundary table in shared memory, strided by the
+// block size (slot j of thread t at [j * blockDim.x + t]): for hash-ordered
+// (sharded) layers, whose warps touch unrelated slots, the local-memory
+// table thrashes L1. Parents with more than kShSlots members use the
+// local-memory table.
+constexpr int kShSlots = 24;
+
+template <int W>
+__device__ __forceinline__ Set<W> candidates_shared(const Set<W>* adj, int k, const Set<W>& S,
+                                                    const Set<W>& eligible, Set<W>* Rsh) {
+    Set<W>* R = Rsh + threadIdx.x;
+    const int stride = blockDim.x;
+    Set<W> rem = S;
+    while (rem.any()) {
+        Set<W> frontier = rem;
+        Set<W> comp = Set<W>::bit(pop_any(frontier));
+        frontier = comp;
+        Set<W> nb = Set<W>::zero();
+        while (frontier.any()) {
+            const Set<W> a = adj[pop_any(frontier)];
+            nb |= a;
+            Set<W> fresh = (a & S) - comp;
+            comp |= fresh;
+            frontier |= fresh;
+        }
+        rem = rem - comp;
+        const Set<W> boundary = nb - S;
+        if (boundary.none()) continue;
+        for_each_any(comp, [&](int u) { R[reach_slot<W, true>(S, u) * stride] = boundary; });
+    }
+    Set<W> keep = Set<W>::zero();
+    for_each_any(eligible, [&](int v) {
+        Set<W> q = adj[v] - S;
+        if (q.count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
+        for_each_any(adj[v] & S, [&](int u) { q |= R[reach_slot<W, true>(S, u) * stride]; });
+        q.del(v);
+        if (q.count() <= k) keep.add(v);
+    });
+    return keep;
+}
+
 template <int W, bool MMW, bool COMPACT = false>
 __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, const Set<W>& S,
-                                             const Set<W>& forbidden, u64& pruned) {
+                                             const Set<W>& forbidden, u64& pruned, Set<W>* Rsh = nullptr) {
     constexpr int N = 64 * W;
     const Set<W> open = Set<W>::prefix(n) - S;
     const Set<W> eligible = open - forbidden;
     Set<W> keep = Set<W>::zero();
     if (eligible.none()) return keep;
+    if constexpr (!MMW) {
+        if (Rsh && S.count() <= kShSlots) return candidates_shared<W>(adj, k, S, eligible, Rsh);
+    }
     Set<W> R[N];
     component_reach<W, COMPACT>(adj, S, R);
     if constexpr (!MMW) {
@@ -361,9 +405,9 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
 template <int W, bool MMW, bool COMPACT = false>
 __device__ __forceinline__ Set<W> warp_candidates(const Set<W>* adj, int n, int k, const Set<W>& S, bool valid,
                                                   const Set<W>& forbidden, u64& pruned,
-                                                  unsigned (*scratch)[2 * W]) {
+                                                  unsigned (*scratch)[2 * W], Set<W>* Rsh = nullptr) {
     u64 unused = 0;
-    Set<W> M = valid ? candidates<W, false, COMPACT>(adj, n, k, S, forbidden, unused) : Set<W>::zero();
+    Set<W> M = valid ? candidates<W, false, COMPACT>(adj, n, k, S, forbidden, unused, Rsh) : Set<W>::zero();
     if constexpr (!MMW) {
         return M;
     } else {
