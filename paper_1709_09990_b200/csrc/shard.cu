@@ -55,6 +55,9 @@ namespace etw {
 namespace {
 
 constexpr int kMaxShards = 8;
+#ifndef ETWG_OWNER_TARGET
+#define ETWG_OWNER_TARGET 640
+#endif
 #ifndef ETWG_ROUTE_COMPACT
 #define ETWG_ROUTE_COMPACT true  // rank-indexed boundary table for hash-ordered layers
 #endif
@@ -64,7 +67,7 @@ constexpr int kRouteThreads = 256;
 template <int W>
 constexpr int owner_slots() { return 2048; }
 template <int W>
-constexpr int owner_target() { return 640; }  // distinct keys aimed for per partition
+constexpr int owner_target() { return ETWG_OWNER_TARGET; }  // distinct keys aimed for per partition
 // Child record: {key words, parent index << 32 | history}. The emission
 // rank (source shard, parent index, vertex) is rebuilt by the owner: the
 // source is the block it reads, the vertex the history's low byte.
