@@ -112,7 +112,7 @@ ELIMTW_API int etwg_shard_exchange_p2p(void);
 /* Layers of up to `states` states are expanded redundantly by every shard on
  * the single-device engine (no routing: cheaper than an exchange for small
  * layers); the first larger layer is split by owner and the decide continues
- * sharded. Default 2^21 (env ETWG_HANDOFF); 0 shards from the root. */
+ * sharded. Default 2^19 (env ETWG_HANDOFF); 0 shards from the root. */
 ELIMTW_API void etwg_set_shard_handoff(uint64_t states);
 
 /* host preprocessing (no GPU needed); rows as above */

@@ -940,7 +940,7 @@ private:
     // split by owner. ETWG_HANDOFF=0 shards from the root.
     u64 handoff_ = [] {
         const char* e = std::getenv("ETWG_HANDOFF");
-        return e ? std::strtoull(e, nullptr, 10) : (u64{1} << 21);
+        return e ? std::strtoull(e, nullptr, 10) : (u64{1} << 19);
     }();
     bool p2p_ = false;          // NCCL mode: pull records over NVLink instead of send/recv
     bool handles_dirty_ = false;  // outboxes (re)allocated since the last handle exchange

@@ -26,7 +26,7 @@ def shards(E, gpu):
         return g
     yield use
     E.set_virtual_shards(1)
-    E.set_shard_handoff(1 << 21)
+    E.set_shard_handoff(1 << 19)
 
 
 def _sets(run):
@@ -203,4 +203,4 @@ def test_nccl_one_rank_communicator(E, gpu):
         assert res.value == 22
     finally:
         E.shard_release()
-        E.set_shard_handoff(1 << 21)
+        E.set_shard_handoff(1 << 19)
