@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
     u64 offered = 0, pruned = 0, winners = 0;
     // Small layer (fewer than 1/8 of the resident threads): one warp per
     // parent, candidates and MMW bounds spread over the lanes.
-    if (E * 8 <= static_cast<u64>(gridDim.x) * blockDim.x) {
+    const bool small = (P->flags & 256) || (!(P->flags & 128) && E * 8 <= static_cast<u64>(gridDim.x) * blockDim.x);
+    if (small) {  // ETWG_DEBUG 128 / 256 force the thread / warp mode (tests)
         Set<W>* R = warp_tables[threadIdx.x >> 5][0];
         Set<W>* rows = warp_tables[threadIdx.x >> 5][MMW ? 1 : 0];
         bool full = false;
