@@ -935,6 +935,7 @@ private:
     u64* d_wit_ = nullptr;
     int pl_round_parity_ = 0;  // buffer holding the current round's input layer
     u64* d_scratch_ = nullptr;  // histogram counters + handoff ticket
+    bool tight_ = std::getenv("ETWG_SHARD_TIGHT") != nullptr;  // tests: force aborts / re-runs
     // layers up to this many states are expanded redundantly by every shard
     // on the single-device engine (no routing); the first larger layer is
     // split by owner. ETWG_HANDOFF=0 shards from the root.
@@ -1178,6 +1179,14 @@ private:
         const u64 per = (routed_max + G_ * pl.np - 1) / (G_ * pl.np);
         pl.cap = std::max<u64>(per + per / 4 + 64, cap_floor_);
         pl.layer_est = per_owner + per_owner / 4 + 1024;
+        if (tight_) {  // tests: undersized plans, so rounds abort, grow and re-run
+            pl.np = std::max<u64>(std::max<u64>(pl.np / 16, 1), np_floor_);
+            pl.lg = 0;
+            while ((u64{1} << pl.lg) < pl.np) ++pl.lg;
+            const u64 per2 = (routed_max + G_ * pl.np - 1) / (G_ * pl.np);
+            pl.cap = std::max<u64>(per2 / 4 + 1, cap_floor_);
+            pl.layer_est = 0;
+        }
         pl.bloom_m = 0;
         if (cfg.dedup == DedupMode::bloom) {
             const u64 cap = host_round_cap(E);
