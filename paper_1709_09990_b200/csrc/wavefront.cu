@@ -152,13 +152,15 @@ __device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C,
         distinct = d < upper ? d : upper;
         winners = w < upper ? w : upper;
     }
+    const bool tight = (P->flags & 1024) != 0;  // tests: undersized plans force aborts / re-runs
     PartPlan pl;
     pl.np = ceil_pow2((distinct + part_target<W>() - 1) / part_target<W>());
+    if (tight) pl.np = pl.np > 16 ? pl.np / 16 : 1;
     if (pl.np < C->part_floor) pl.np = C->part_floor;
     pl.lg = 0;
     while ((u64{1} << pl.lg) < pl.np) ++pl.lg;
     const u64 per = (winners + pl.np - 1) / pl.np;
-    pl.cap = per + per / 4 + 64;
+    pl.cap = tight ? per / 4 + 1 : per + per / 4 + 64;
     if (pl.cap < C->rec_floor) pl.cap = C->rec_floor;
     return pl;
 }

@@ -349,3 +349,23 @@ def test_scatter_thread_and_warp_modes_agree(gpu):
     thread = _run_with_debug(128, _MODES_CODE)
     warp = _run_with_debug(256, _MODES_CODE)
     assert thread == warp
+
+
+_TIGHT_CODE = """
+import json, sys
+sys.path.insert(0, ".")
+from paper_1709_09990_b200 import elimtw as E, generators as G
+res = {}
+for name, rows, k, mmw in (("g", G.random_graph(1, 40, 0.3), 21, False), ("q", G.queen_graph(5, 5), 18, True),
+                           ("w", G.random_graph(9, 70, 0.07), 5, False)):
+    r = E.decide(rows, k, dedup="exact", mmw=mmw, rounds=8 if name == "w" else -1)
+    res[name] = [r.outcome, r.witness_set, r.witness_hist, [x.tuple() for x in r.rounds], r.layers]
+print(json.dumps(res))
+"""
+
+
+def test_partitioned_rounds_survive_aborts(gpu):
+    """Undersized bucket plans (ETWG_DEBUG 1024: 1/16 of the partitions, 1/4
+    of the record capacity) make rounds abort and re-run with raised floors;
+    exact layers, orders, histories and counters are unchanged."""
+    assert _run_with_debug(1024, _TIGHT_CODE) == _run_with_debug(0, _TIGHT_CODE)
