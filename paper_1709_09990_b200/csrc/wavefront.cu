@@ -121,10 +121,14 @@ __device__ __forceinline__ bool halted(const Control* C) {
 // Bucket count and capacity are planned on the device from the previous
 // round's growth; an overflow aborts the round and raises the floor.
 
+#ifndef ETWG_PART_DIV
+#define ETWG_PART_DIV 3  // table slots per targeted distinct key
+#endif
+
 template <int W>
 constexpr int part_slots() { return W == 1 ? 4096 : 2048; }
 template <int W>
-constexpr int part_target() { return part_slots<W>() / 3; }  // distinct keys aimed for per bucket
+constexpr int part_target() { return part_slots<W>() / ETWG_PART_DIV; }  // distinct keys aimed for per bucket
 template <int W>
 constexpr int rec_words() { return W == 1 ? 2 : 4; }  // {key, rank} / {lo, hi, rank, pad}
 template <int W>

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q --timeout 900 -k "survive" > gpurun_out/tight1.txt 2>&1; tail -3 gpurun_out/tight1.txt
+for v in "" _pd2 _pd4; do echo "variant $v"; ETWG_LIB=paper_1709_09990_b200/libelimtw$v.so timeout 300 python tools/prof_g48.py exact 2>&1 | sed -n 1p; ETWG_LIB=paper_1709_09990_b200/libelimtw$v.so timeout 300 python tools/prof_g48.py exact 2>&1 | grep insert_ms; done
