@@ -1,7 +1,8 @@
 """Per-config measurements (not the bench line): every BASELINE.json config on
 one B200 beside the reference CPU solver (oracle/_ref) on the same box.
 Writes profiles/<out>.json and prints a markdown table.
-Usage: python tools/configs_table.py out_name [ref_threads]
+Test infrastructure (uses the reference build as the CPU arm).
+Usage: python tests/measure_configs.py out_name [ref_threads]
 
   cfg1  myciel4, exact, default options (1 GPU vs reference 1 thread and all)
   cfg2  queen6_6, --mmw, Bloom
@@ -16,7 +17,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # tests/ -> repo
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 from paper_1709_09990_b200 import elimtw as E, generators as G  # noqa: E402
