@@ -1,13 +1,6 @@
 mkdir -p gpurun_out
-cat > /tmp/w2.py <<'PY'
-import os, sys, json
-sys.path.insert(0, os.getcwd())
-from paper_1709_09990_b200 import elimtw as E, generators as G
-g = E.Graph.from_rows(G.grid_with_chords(8, 9, 6, 7))
-o = E.Options(dedup="exact")
-E.solve(g, o)
-E.timer_begin(); r = E.solve(g, o); ms = E.timer_end()
-print(r.kind, r.value, f"{ms:.1f} ms", json.loads(r.stats_json)["totals"]["expanded"])
-PY
-python /tmp/w2.py
-ETWG_LIB=paper_1709_09990_b200/libelimtw_w2c.so python /tmp/w2.py
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/final_tests.txt 2>&1; tail -2 gpurun_out/final_tests.txt
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; tail -1 gpurun_out/bench_final.err
+python -c "import json; d=json.load(open('gpurun_out/bench_final.json')); print(d['value'], d['ms_per_step'], d['e2e']['value'], round(d['roofline']['frac'],4), d['cpu_baseline']['value'], d['clocks'])"
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; tail -c 300 gpurun_out/bench_ref.json
