@@ -121,6 +121,9 @@ __device__ __forceinline__ bool halted(const Control* C) {
 // Bucket count and capacity are planned on the device from the previous
 // round's growth; an overflow aborts the round and raises the floor.
 
+#ifndef ETWG_SCATTER_COMPACT
+#define ETWG_SCATTER_COMPACT false  // vertex-indexed boundary table (rank order keeps it L1-friendly)
+#endif
 #ifndef ETWG_PART_DIV
 #define ETWG_PART_DIV 3  // table slots per targeted distinct key
 #endif
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
         const u64 idx = base + lane;
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        const Set<W> M = warp_candidates<W, MMW>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
+        const Set<W> M = warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         offered += M.count();
         winners += M.count();
         if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bloom_dedup(const Params* __res
         const u64 idx = base + lane;
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        const Set<W> M = warp_candidates<W, MMW>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
+        const Set<W> M = warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         offered += M.count();
         for (unsigned i = lane; i < kWarpSlots * W; i += 32) my_slots[i] = 0;
 #pragma unroll

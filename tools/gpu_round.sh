@@ -1,6 +1,2 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/final_tests.txt 2>&1; tail -2 gpurun_out/final_tests.txt
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; tail -1 gpurun_out/bench_final.err
-python -c "import json; d=json.load(open('gpurun_out/bench_final.json')); print(d['value'], d['ms_per_step'], d['e2e']['value'], round(d['roofline']['frac'],4), d['cpu_baseline']['value'], d['clocks'])"
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; tail -c 300 gpurun_out/bench_ref.json
+for v in "" _sc; do echo "variant $v"; ETWG_LIB=paper_1709_09990_b200/libelimtw$v.so timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | sed -n 2p; ETWG_LIB=paper_1709_09990_b200/libelimtw$v.so timeout 300 python tools/prof_g48.py exact 2>&1 | sed -n 1p; done
