@@ -1,31 +1,37 @@
 // B200 (sm_100a) wavefront engine: the device replacement for the reference's
 // decide / expand_layer / expand_range / q_set / ConcurrentBloom / MMW hot
 // path (proj/src/dp.cpp:23-194, graph.hpp:61-78, bloom.cpp:27-125,
-// mmw.cpp:20-146).
+// mmw.cpp:20-146) on one GPU. (shard.cu runs the same rounds owner-sharded
+// over several GPUs.)
 //
 // Per round (one BFS layer of the Held-Karp prefix DP) the device runs:
-//   bloom : k_bloom_dedup -> k_append<mask>
-//   exact : k_exact_scatter -> k_exact_part -> k_append
+//   exact                  : k_exact_scatter -> k_exact_part -> k_append
+//   bloom, filter > 2^28 b : k_exact_scatter<BLOOM> -> k_exact_part<BLOOM> -> k_append
+//   bloom, smaller filters : k_bloom_dedup -> k_append
 //
-//   candidates     one thread per parent S. The components of G[S] are
-//                  flood-filled once with bitmask ops; Q(S,v) for every
-//                  candidate is then the union of v's outside neighbours and
-//                  the outside boundary of every component v touches
-//                  (children that pass |Q| <= k and, when enabled, the
-//                  minor-min-width bound). Identical children of one tile of
-//                  parents are resolved in shared memory first (tile_dedup).
-//   k_*_insert     children are flattened across the warp (warp scan +
-//                  shuffle binary search), so the atomic-heavy dedup runs one
-//                  child per lane. Bloom: 32-bit atomicOr on the reference's
-//                  bit positions, striped lock on h1 % 65536 for exactly-once
-//                  novelty, warp pre-dedup. Exact: children hash-partitioned
-//                  into buckets whose distinct keys fit a shared-memory
-//                  open-addressing table (CAS claim + atomicMin on the rank).
-//   k_append       single-pass decoupled look-back scan over tiles of
-//                  parents; survivors are written in rank order (parent index
-//                  major, vertex minor) so exact mode reproduces the
-//                  reference's sorted-by-first-emission layer byte for byte
-//                  (dp.cpp:140-157), including truncation at the capacity wall.
+//   candidates       (K1, wave_device.cuh) one thread per parent S — one warp
+//                    per parent on small layers. The components of G[S] are
+//                    flood-filled once with bitmask ops; Q(S,v) for every
+//                    candidate is the union of v's outside neighbours and the
+//                    outside boundary of every component v touches; with MMW
+//                    the surviving children's minor-min-width bounds are
+//                    spread over the warp.
+//   k_exact_scatter  K1 + every child {key, rank} appended to the bucket of
+//                    its key hash (buckets sized so one bucket's distinct
+//                    keys fit a shared-memory table).
+//   k_exact_part     one CTA per bucket: min emission rank per key in shared
+//                    memory (CAS claim + atomicMin), one atomicOr per distinct
+//                    key marks its min-rank child in the parent's mask (BLOOM:
+//                    the key must first pass the reference's filter).
+//   k_bloom_dedup    K1 + the reference's Bloom filter on every child
+//                    (32-bit atomicOr on its bit positions, exactly-once
+//                    novelty through an epoch-tagged claim table).
+//   k_append         single-pass decoupled look-back scan over tiles of 2048
+//                    parents; marked children are written in rank order
+//                    (parent index major, vertex minor) so exact mode
+//                    reproduces the reference's sorted-by-first-emission layer
+//                    byte for byte (dp.cpp:140-157), including truncation at
+//                    the capacity wall.
 //
 // All per-round sizes live in device memory (Control), so the host enqueues
 // rounds without synchronising; it checks the control block once per chunk.
