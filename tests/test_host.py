@@ -159,3 +159,25 @@ def test_golden_stats_are_reference_schema(goldens):
     s = json.loads(goldens["instances"]["myciel4"]["exact_stats"])
     assert s["schema_version"] == 1 and s["result"]["value"] == 10
     assert s["totals"]["expanded"] == 86786
+
+
+def test_shard_api_validates_arguments_without_a_device(E):
+    """The sharding seam (elimtw_gpu.h) rejects bad arguments before touching
+    a device or NCCL, with the reference's error classes; without sharding
+    the process stays on the single-device engine."""
+    from paper_1709_09990_b200 import distributed as D
+    assert E.shard_info() == {"world": 1, "rank": 0, "virtual": False, "p2p": False}
+    for bad in (0, 9, -1):
+        with pytest.raises(ValueError):
+            E.set_virtual_shards(bad)
+    uid = E.nccl_unique_id()  # needs libnccl, not a GPU
+    assert len(uid) == 128
+    with pytest.raises(ValueError):
+        E.shard_init(uid, 2, 2, 0)  # rank out of range
+    with pytest.raises(ValueError):
+        E.shard_init(uid, 0, 9, 0)  # world too large
+    with pytest.raises(ValueError):
+        E.shard_init(b"x" * 10, 0, 2, 0)  # not an ncclUniqueId
+    E.set_virtual_shards(1)  # "off" is always accepted
+    assert D.init_shards() == E.shard_info()  # world 1 (no torchrun env): a no-op
+    assert E.shard_info()["world"] == 1
