@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-for v in "" _sc; do echo "variant $v"; ETWG_LIB=paper_1709_09990_b200/libelimtw$v.so timeout 300 python tools/prof_decide.py 22 exact 2 2>&1 | sed -n 2p; ETWG_LIB=paper_1709_09990_b200/libelimtw$v.so timeout 300 python tools/prof_g48.py exact 2>&1 | sed -n 1p; done
+timeout 1200 python tests/fuzz_device.py 600 7 > gpurun_out/fuzz.txt 2>&1; tail -15 gpurun_out/fuzz.txt
