@@ -86,6 +86,7 @@ DecideResult device_decide_prefix(const Graph& g, int k, const HostSet& forbidde
                                   int rounds, const LayerObserver* observer, uint64_t handoff_above,
                                   EngineLayer& handoff);
 int engine_device();  // the single-device engine's CUDA device (-1 without one)
+void engine_release_buffers();  // frees the single-device engine's round buffers
 
 struct ExpandResult {
     std::vector<State> states;

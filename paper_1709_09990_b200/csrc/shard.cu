@@ -658,6 +658,7 @@ public:
         if (G == 1) return;
         int dev = 0;
         if (const char* e = std::getenv("ETWG_DEVICE")) dev = std::atoi(e);
+        engine_release_buffers();  // the shards take over the device's HBM
         init_device(dev);
         G_ = G;
         local_.resize(G);
@@ -669,6 +670,7 @@ public:
         if (rank < 0 || rank >= world) throw std::invalid_argument("rank out of range");
         release();
         Nccl& nc = Nccl::get();
+        engine_release_buffers();
         init_device(device);
         ncclUniqueId uid;
         std::memcpy(&uid, id, sizeof uid);

@@ -849,6 +849,34 @@ public:
         return out;
     }
 
+    // Frees every round buffer (they are re-grown on demand): the sharded
+    // engine calls this when it takes over the device, so a process that
+    // solved a large instance on one GPU does not keep that HBM.
+    void release_buffers() {
+        if (init_state_ != 1) return;
+        check(cudaStreamSynchronize(stream_), "sync");
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(b_.keys[i]);
+            cudaFree(b_.hist[i]);
+            cudaFree(b_.bloom[i]);
+            b_.keys[i] = nullptr;
+            b_.hist[i] = nullptr;
+            b_.bloom[i] = nullptr;
+            bloom_dirty_[i] = 0;
+        }
+        cudaFree(b_.cmask);
+        cudaFree(b_.tiles);
+        cudaFree(b_.recs);
+        cudaFree(b_.cursors);
+        cudaFree(b_.claims);
+        b_.cmask = nullptr;
+        b_.tiles = nullptr;
+        b_.recs = nullptr;
+        b_.cursors = nullptr;
+        b_.claims = nullptr;
+        b_.layer_cap = b_.rec_cap = b_.cursor_cap = b_.bloom_cap = b_.claim_cap = 0;
+    }
+
     uint64_t bloom_batch(uint64_t expected, int bpe, int hashes, const std::vector<uint64_t>& keys,
                          int words, std::vector<uint8_t>& novel, std::vector<uint32_t>* bits) {
         require_device();
@@ -1415,6 +1443,12 @@ DecideResult device_decide_prefix(const Graph& g, int k, const HostSet& forbidde
     std::lock_guard<std::mutex> lock(e.mu);
     handoff.handed = false;
     return e.decide(g, k, forbidden, cfg, rounds, observer, handoff_above, &handoff);
+}
+
+void engine_release_buffers() {
+    Engine& e = Engine::instance();
+    std::lock_guard<std::mutex> lock(e.mu);
+    e.release_buffers();
 }
 
 int engine_device() {
