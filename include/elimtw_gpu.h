@@ -114,6 +114,11 @@ ELIMTW_API int etwg_shard_exchange_p2p(void);
  * layers); the first larger layer is split by owner and the decide continues
  * sharded. Default 2^19 (env ETWG_HANDOFF); 0 shards from the root. */
 ELIMTW_API void etwg_set_shard_handoff(uint64_t states);
+/* 1 (default): each next-layer state stays on the shard that emitted its
+ * winning (min-rank) child — the owner only deduplicates and returns a mark,
+ * layers stay rank-ordered per shard; 0: states move to their hash owner
+ * (env ETWG_SHARD_MODE=owner). The NCCL send/recv fallback always uses 0. */
+ELIMTW_API void etwg_set_shard_mode(int emitter);
 
 /* host preprocessing (no GPU needed); rows as above */
 ELIMTW_API void etwg_graph_rows(const etw_graph* g, uint64_t* rows);

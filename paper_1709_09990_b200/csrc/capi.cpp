@@ -472,6 +472,13 @@ void etwg_shard_release(void) {
     }
 }
 
+void etwg_set_shard_mode(int emitter) {
+    try {
+        shard_set_mode(emitter);
+    } catch (...) {
+    }
+}
+
 void etwg_set_shard_handoff(uint64_t states) {
     try {
         shard_set_handoff(states);

@@ -152,6 +152,8 @@ void shard_info(int* world, int* rank, int* virt);
 int shard_p2p();  // 1 when the NCCL path pulls records over NVLink (CUDA IPC)
 // layers up to `states` run replicated on the single-device engine (0: shard from the root)
 void shard_set_handoff(uint64_t states);
+// 1: next-layer states stay on their emitting shard (default); 0: on their hash owner
+void shard_set_mode(int emitter);
 void shard_timer_begin();
 double shard_timer_end();
 void shard_accumulate(KernelTimes& t);

@@ -82,11 +82,11 @@ __device__ __forceinline__ u64 owner_rank(int src, u64 packed) {
     return (static_cast<u64>(src) << 40) | ((packed >> 32) << 7) | (packed & 0x7F);
 }
 
-enum ShardAbort : unsigned { kAbortLayer = 1, kAbortRecs = 2, kAbortParts = 4 };
+enum ShardAbort : unsigned { kAbortLayer = 1, kAbortRecs = 2, kAbortParts = 4, kAbortMarks = 8 };
 
 struct ShardStat {
     u64 expanded, offered, pruned, routed, unique;
-    u64 need_layer, need_recs, need_parts;
+    u64 need_layer, need_recs, need_parts, need_marks;
     unsigned abort, pad;
 };
 
@@ -113,6 +113,7 @@ struct Plan {
     u64 layer_est;  // host sizing hint: next-layer states per owner
     int lg, G, me, rounds;
     int shared_r;   // k_route keeps K1's boundary tables in (dynamic) shared memory
+    int emit;       // emitter-stored layers: records carry (index << 7 | vertex), no history
 };
 
 struct ShardBufs {
@@ -138,6 +139,15 @@ struct ShardBufs {
     u64 stage_cap;       // partitions the staging holds
     unsigned* bloom;     // the owner's Bloom slice (32-bit words)
     u64 bloom_cap;       // words
+    // emitter-stored layers (ETWG_SHARD_MODE=emitter): winner marks the
+    // owner returns to each emitting shard, [emitter][mark_cap] of
+    // (parent index << 7 | vertex), and the emitter's parent winner masks
+    u64* marks;
+    unsigned* mark_cnt;  // [emitter]
+    u64 mark_cap;        // marks per emitter
+    const u64* src_marks[kMaxShards];       // owner o's marks for this shard
+    const unsigned* src_mark_cnt[kMaxShards];
+    u64* cmask;          // u64[W] per local parent
 };
 
 template <int W>
@@ -196,6 +206,7 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
             adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep,
             (!TILE && !MMW && W == 1 && pl.shared_r) ? reinterpret_cast<Set<W>*>(smem_raw) : nullptr);
         offered += M.count();
+        if (pl.emit && valid) store_set<W>(B.cmask, idx, Set<W>::zero());
         if constexpr (TILE) {
             tile_set_clear<W, route_tile_slots<W>()>(ts);
             __syncthreads();
@@ -220,7 +231,8 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
                 const unsigned slot = atomicAdd(B.out_cnt + bucket, 1u);
                 if (slot < pl.cap) {
                     u64* rec = B.out + (bucket * pl.cap + slot) * srec_words<W>();
-                    const u64 packed = ((warp_base + src) << 32) | ((Hs << 8) | static_cast<unsigned>(v));  // push_history
+                    const u64 packed = pl.emit ? (((warp_base + src) << 7) | static_cast<u64>(v))
+                                               : (((warp_base + src) << 32) | ((Hs << 8) | static_cast<unsigned>(v)));  // push_history
                     if constexpr (W == 1) {
                         *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], packed);
                     } else {
@@ -469,6 +481,214 @@ __global__ void __launch_bounds__(kRouteThreads) k_owner_compact(ShardCtl* C, Sh
 }
 
 // ----------------------------------------------------------------------
+// Emitter-stored layers. The owner of a key only deduplicates it: of all
+// emissions it keeps one winner — the emitting shard closest after the owner
+// in cyclic order (so every shard stores about its share), then the smallest
+// (parent index, vertex) there — and returns a mark to that emitter, which
+// keeps the state in its own next layer. Layers stay in rank order on every
+// shard, histories are computed where the parent lives, and the owner
+// neither sorts nor stages.
+
+template <int W, bool BLOOM>
+__global__ void __launch_bounds__(kOwnerThreads) k_owner_emit(const Params* __restrict__ P, ShardCtl* C,
+                                                              ShardBufs B, Plan pl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int SLOTS = owner_slots<W>();
+    u64* ranks = reinterpret_cast<u64*>(smem_raw);
+    u64* keys = ranks + SLOTS;
+    __shared__ unsigned s_full, s_cnt[kMaxShards], s_pos[kMaxShards];
+    __shared__ u64 s_part, s_base[kMaxShards];
+    if (C->stop) return;
+    for (;;) {
+        if (threadIdx.x == 0) s_part = atomicAdd(&C->ticket, 1ull);
+        __syncthreads();
+        const u64 part = s_part;
+        if (part >= pl.np) break;
+        for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) keys[i] = 0;
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) ranks[i] = ~u64{0};
+        if (threadIdx.x < kMaxShards) {
+            s_cnt[threadIdx.x] = 0;
+            s_pos[threadIdx.x] = 0;
+        }
+        if (threadIdx.x == 0) s_full = 0;
+        __syncthreads();
+        for (int s = 0; s < pl.G; ++s) {
+            const u64 pri = static_cast<u64>((s - pl.me + pl.G) % pl.G) << 40;
+            const unsigned cnt = min(B.src_cnt[s][part], static_cast<unsigned>(pl.cap));
+            const u64* recs = B.src_recs[s] + part * pl.cap * srec_words<W>();
+            for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
+                Set<W> key;
+                u64 packed;
+                load_srec<W>(recs + static_cast<u64>(i) * srec_words<W>(), key, packed);
+                unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
+                bool placed = false;
+                for (int probe = 0; probe < SLOTS && !placed; ++probe) {
+                    placed = smem_claim<W>(keys, h, key);
+                    if (!placed) h = (h + 1) & (SLOTS - 1);
+                }
+                if (placed)
+                    atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), pri | packed);
+                else
+                    s_full = 1;
+            }
+        }
+        __syncthreads();
+        if (s_full) {
+            if (threadIdx.x == 0) {
+                atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortParts));
+                atomicMax(&C->mine.need_parts, 2 * pl.np);
+            }
+            __syncthreads();
+            continue;
+        }
+        // winners (Bloom: those the owner's filter calls novel) -> marks
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+                const u64 rank = ranks[i];
+                if (rank == ~u64{0}) continue;
+                if constexpr (BLOOM) {
+                    if (pass == 0) {
+                        Set<W> key;
+#pragma unroll
+                        for (int w = 0; w < W; ++w) key.w[w] = keys[W * i + w];
+                        const unsigned h1 = murmur_key<W>(key, kSeed1);
+                        const unsigned h2 = murmur_key<W>(key, kSeed2);
+                        u64 pos, step;
+                        probe_start(h1, h2, pl.bloom_m, pos, step);
+                        bool novel = false;
+                        for (int t = 1; t <= P->hashes; ++t) {
+                            const unsigned bit = 1u << (pos & 31);
+                            novel |= (atomicOr(B.bloom + (pos >> 5), bit) & bit) == 0;
+                            pos += step;
+                            if (pos >= pl.bloom_m) pos -= pl.bloom_m;
+                        }
+                        if (!novel) {
+                            ranks[i] = ~u64{0};  // a false positive: dropped as the reference drops it
+                            continue;
+                        }
+                    }
+                }
+                const int emitter = static_cast<int>(((rank >> 40) + pl.me) % pl.G);
+                if (pass == 0) {
+                    atomicAdd(&s_cnt[emitter], 1u);
+                } else {
+                    const u64 slot = s_base[emitter] + atomicAdd(&s_pos[emitter], 1u);
+                    if (slot < B.mark_cap) B.marks[emitter * B.mark_cap + slot] = rank & ((u64{1} << 40) - 1);
+                }
+            }
+            __syncthreads();
+            if (pass == 0 && threadIdx.x < pl.G) {
+                const unsigned c = s_cnt[threadIdx.x];
+                s_base[threadIdx.x] = c ? atomicAdd(B.mark_cnt + threadIdx.x, c) : 0;
+                if (c && s_base[threadIdx.x] + c > B.mark_cap) {
+                    atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortMarks));
+                    atomicMax(&C->mine.need_marks, 2 * B.mark_cap);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// marks from every owner -> this shard's parents' winner masks
+template <int W>
+__global__ void k_apply_marks(ShardCtl* C, ShardBufs B, Plan pl) {
+    if (C->stop) return;
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (int o = 0; o < pl.G; ++o) {
+        const u64 cnt = min(static_cast<u64>(B.src_mark_cnt[o][pl.me]), B.mark_cap);
+        const u64* marks = B.src_marks[o] + static_cast<u64>(pl.me) * B.mark_cap;
+        for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < cnt; i += stride) {
+            const u64 m = __ldcs(marks + i);
+            const u64 idx = m >> 7;
+            const int v = static_cast<int>(m & 127);
+            atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + idx * W + (v >> 6), u64{1} << (v & 63));
+        }
+    }
+}
+
+// marked children -> this shard's next layer in rank order (tiles of 2048
+// parents, one decoupled look-back per tile; histories pushed here)
+template <int W>
+__global__ void __launch_bounds__(kRouteThreads) k_emit_append(ShardCtl* C, ShardBufs B, Plan pl) {
+    using BlockScan = cub::BlockScan<unsigned, kRouteThreads>;
+    constexpr int ITEMS = W == 1 ? 8 : 4;
+    constexpr u64 kSpan = static_cast<u64>(kRouteThreads) * ITEMS;
+    __shared__ typename BlockScan::TempStorage scan_tmp;
+    __shared__ u64 s_prefix, s_tile;
+    if (C->stop) return;
+    const unsigned r = C->round;
+    const unsigned epoch = C->epoch;
+    const u64 E = C->count[r & 1];
+    const u64 ntiles = (E + kSpan - 1) / kSpan;
+    const u64* in = B.keys[r & 1];
+    const unsigned* hin = B.hist[r & 1];
+    u64* out = B.keys[(r + 1) & 1];
+    unsigned* hout = B.hist[(r + 1) & 1];
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&C->ticket2, 1ull);
+        __syncthreads();
+        const u64 tile = s_tile;
+        if (tile >= ntiles) break;
+        Set<W> S[ITEMS], M[ITEMS];
+        unsigned H[ITEMS], excl[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const u64 idx = tile * kSpan + static_cast<u64>(i) * kRouteThreads + threadIdx.x;
+            const bool valid = idx < E;
+            S[i] = valid ? load_set<W>(in, idx) : Set<W>::zero();
+            H[i] = valid ? hin[idx] : 0u;
+            M[i] = valid ? load_set<W>(B.cmask, idx) : Set<W>::zero();
+        }
+        unsigned total = 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            unsigned slice_total;
+            BlockScan(scan_tmp).ExclusiveSum(static_cast<unsigned>(M[i].count()), excl[i], slice_total);
+            excl[i] += total;
+            total += slice_total;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) s_prefix = look_back(B.tiles, tile, total, epoch);
+        __syncthreads();
+        const u64 prefix = s_prefix;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const Set<W> Mi = M[i];
+            WarpFlat f;
+            f.scan(Mi.count());
+            const u64 warp_start = prefix + __shfl_sync(kFull, excl[i], 0);
+            for (int t = 0; t < f.total; t += 32) {
+                const int j = t + lane;
+                const int src = f.source(j);
+                const int ex = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
+                const Set<W> Ms = shfl_set<W>(Mi, src);
+                const Set<W> Ss = shfl_set<W>(S[i], src);
+                const unsigned Hs = __shfl_sync(kFull, H[i], src);
+                const u64 pos = warp_start + j;
+                if (j < f.total && pos < B.layer_cap) {
+                    const int v = nth_member<W>(Ms, j - ex);
+                    Set<W> key = Ss;
+                    key.add(v);
+                    store_set<W>(out, pos, key);
+                    hout[pos] = (Hs << 8) | static_cast<unsigned>(v & 0xFF);  // push_history
+                }
+            }
+        }
+        if (threadIdx.x == 0 && tile == ntiles - 1) {
+            const u64 unique = prefix + total;
+            C->mine.unique = unique;
+            if (unique > B.layer_cap) {
+                atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortLayer));
+                atomicMax(&C->mine.need_layer, unique);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------------
 // Handoff from the replicated prefix: every rank holds the whole layer (in
 // rank order); each keeps the states it owns, in the same order.
 
@@ -637,6 +857,8 @@ struct Shard {
     u64 bloom_dirty = 0;  // words of the Bloom slice that may hold bits
     int box_words = 0;    // W the boxes were sized for
     int stage_words = 0;  // W the owner staging was sized for
+    u64 mark_alloc = 0;   // emitter mode: marks allocated
+    u64 cmask_cap = 0;    // emitter mode: parents the winner masks cover
 };
 
 class ShardSet {
@@ -699,6 +921,8 @@ public:
     }
 
     void set_handoff(u64 states) { handoff_ = states; }
+    void set_mode(int emitter) { emit_request_ = emitter != 0; }
+    int mode() const { return emit_request_ ? 1 : 0; }
     u64 handoff() const { return handoff_; }
 
     // exchange mode of the NCCL path: 1 = owners read peers' outboxes over
@@ -753,6 +977,8 @@ public:
         check(cudaEventRecord(ev_[0], stream_), "event");
         np_floor_ = 1;
         cap_floor_ = 0;
+        mark_floor_ = 0;
+        emit_ = emit_request_ && (!comm_ || p2p_);
         const bool bloom = cfg.dedup == DedupMode::bloom;
         // host mirror of the global round state
         std::vector<u64> count(G_, 0);
@@ -781,7 +1007,11 @@ public:
             prev.unique = last.emitted;
             prev.routed = last.emitted + last.duplicates;
             prev.emitted = last.emitted;
-            count = owner_counts(lay);
+            if (emit_) {  // any split works: contiguous slices keep rank order
+                for (int q = 0; q < G_; ++q) count[q] = lay.count * (q + 1) / G_ - lay.count * q / G_;
+            } else {
+                count = owner_counts(lay);
+            }
             for (Shard& s : local_) setup(s, g, k, forbidden, cfg, rounds, r, &lay, count[s.me]);
         } else {
             for (Shard& s : local_) setup(s, g, k, forbidden, cfg, rounds);
@@ -790,7 +1020,7 @@ public:
         const int r_first = r;
         bool stopped = false;
         while (r < rounds && !stopped) {
-            const Plan pl = plan(r, count, prev, cfg, W);
+            Plan pl = plan(r, count, prev, cfg, W);
             pl_round_parity_ = r & 1;
             if (trace_)
                 std::fprintf(stderr, "[shard] k=%d r=%d E=%llu np=%llu cap=%llu recs/shard=%llu prev(exp=%llu routed=%llu uniq=%llu)\n",
@@ -804,13 +1034,21 @@ public:
             for (Shard& s : local_) prepare_round(s, pl, W, bloom, count);
             if (comm_ && p2p_ && handles_dirty_) {
                 share_outboxes(local_[0]);
-                if (!p2p_)  // a peer mapping failed on some rank: NCCL exchange from here on
+                if (!p2p_) {  // a peer mapping failed on some rank: NCCL exchange, owner-stored layers
+                    pl = plan(r, count, prev, cfg, W);
                     for (Shard& s : local_) prepare_round(s, pl, W, bloom, count);
+                }
             }
             for (Shard& s : local_) launch_route(s, pl, W, cfg.use_mmw);
             exchange(pl, W);
-            for (Shard& s : local_) launch_owner(s, pl, W, bloom);
-            for (Shard& s : local_) launch_compact(s, pl, W);
+            if (emit_) {
+                for (Shard& s : local_) launch_owner_emit(s, pl, W, bloom);
+                if (comm_) route_barrier();  // every owner's marks are complete
+                for (Shard& s : local_) launch_emit_append(s, pl, W);
+            } else {
+                for (Shard& s : local_) launch_owner(s, pl, W, bloom);
+                for (Shard& s : local_) launch_compact(s, pl, W);
+            }
             allgather_stats();
             for (Shard& s : local_) {
                 Plan p = pl;
@@ -836,6 +1074,11 @@ public:
             }
             if (abort) {
                 if (abort & kAbortRecs) cap_floor_ = std::max(cap_floor_, need_recs);
+                if (abort & kAbortMarks) {
+                    u64 need_marks = 0;
+                    for (int q = 0; q < G_; ++q) need_marks = std::max(need_marks, c0.all[q].need_marks);
+                    mark_floor_ = std::max(mark_floor_, need_marks);
+                }
                 if (abort & kAbortParts) np_floor_ = std::max(np_floor_, need_parts);
                 for (Shard& s : local_) {
                     if (abort & kAbortLayer) grow_layers(s, need_layer + need_layer / 2, r & 1, count[s.me]);
@@ -847,6 +1090,7 @@ public:
             prev = c0.rs[r];
             np_floor_ = 1;  // floors only widen the round that overflowed
             cap_floor_ = 0;
+            mark_floor_ = 0;
             // every shard's kept count, shard-major (as k_shard_finish computed it)
             const u64 cap = host_round_cap(prev.expanded);
             u64 before = 0;
@@ -938,6 +1182,17 @@ private:
     int pl_round_parity_ = 0;  // buffer holding the current round's input layer
     u64* d_scratch_ = nullptr;  // histogram counters + handoff ticket
     bool tight_ = std::getenv("ETWG_SHARD_TIGHT") != nullptr;  // tests: force aborts / re-runs
+    // Emitter-stored layers (default; ETWG_SHARD_MODE=owner or
+    // etwg_set_shard_mode(0) selects owner-stored): next-layer states stay
+    // on the shard that emitted them, owners only deduplicate and return
+    // marks. Virtual shards and the NVLink pull; the NCCL send/recv exchange
+    // keeps owner-stored layers.
+    bool emit_request_ = [] {
+        const char* e = std::getenv("ETWG_SHARD_MODE");
+        return !(e && std::strcmp(e, "owner") == 0);
+    }();
+    bool emit_ = false;
+    u64 mark_cap_plan_ = 0, mark_floor_ = 0;
     // layers up to this many states are expanded redundantly by every shard
     // on the single-device engine (no routing); the first larger layer is
     // split by owner. ETWG_HANDOFF=0 shards from the root.
@@ -949,6 +1204,8 @@ private:
     bool handles_dirty_ = false;  // outboxes (re)allocated since the last handle exchange
     const u64* peer_out_[kMaxShards] = {};
     const unsigned* peer_cnt_[kMaxShards] = {};
+    const u64* peer_marks_[kMaxShards] = {};
+    const unsigned* peer_mark_cnt_[kMaxShards] = {};
     unsigned char* d_handles_ = nullptr;
 
     void init_device(int dev) {
@@ -973,6 +1230,13 @@ private:
         allow(k_owner<1, true>, owner_smem_bytes<1>(), grid_owner_[0]);
         allow(k_owner<2, false>, owner_smem_bytes<2>(), grid_owner_[1]);
         allow(k_owner<2, true>, owner_smem_bytes<2>(), grid_owner_[1]);
+        {
+            int g;
+            allow(k_owner_emit<1, false>, owner_smem_bytes<1>(), g);
+            allow(k_owner_emit<1, true>, owner_smem_bytes<1>(), g);
+            allow(k_owner_emit<2, false>, owner_smem_bytes<2>(), g);
+            allow(k_owner_emit<2, true>, owner_smem_bytes<2>(), g);
+        }
         auto allow_route = [&](auto kernel, int bytes, int& grid) {
             check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem");
             int blocks = 0;
@@ -1039,6 +1303,9 @@ private:
         cudaFree(s.b.stage);
         cudaFree(s.b.stage_hist);
         cudaFree(s.b.pcount);
+        cudaFree(s.b.marks);
+        cudaFree(s.b.mark_cnt);
+        cudaFree(s.b.cmask);
         s = Shard{};
     }
 
@@ -1074,7 +1341,16 @@ private:
             c.round = static_cast<unsigned>(r0);
             c.count[r0 & 1] = owned;
             grow_layers(s, owned + owned / 4 + 1024, 0, 0);
-            take_owned(s, *from, r0 & 1);
+            if (emit_) {
+                const u64 first = from->count * static_cast<u64>(s.me) / G_;
+                const int W = from->W;
+                check(cudaMemcpyAsync(s.b.keys[r0 & 1], static_cast<const u64*>(from->keys) + first * W, owned * 8 * W,
+                                      cudaMemcpyDeviceToDevice, stream_), "handoff slice");
+                check(cudaMemcpyAsync(s.b.hist[r0 & 1], from->hist + first, owned * 4, cudaMemcpyDeviceToDevice, stream_),
+                      "handoff slice");
+            } else {
+                take_owned(s, *from, r0 & 1);
+            }
             check(cudaMemcpyAsync(s.d_ctl, s.h_ctl, sizeof(ShardCtl), cudaMemcpyHostToDevice, stream_), "control");
             return;
         }
@@ -1181,6 +1457,8 @@ private:
         const u64 per = (routed_max + G_ * pl.np - 1) / (G_ * pl.np);
         pl.cap = std::max<u64>(per + per / 4 + 64, cap_floor_);
         pl.layer_est = per_owner + per_owner / 4 + 1024;
+        pl.emit = emit_ ? 1 : 0;
+        mark_cap_plan_ = std::max<u64>(per_owner + per_owner / 2 + 4096, mark_floor_);
         if (tight_) {  // tests: undersized plans, so rounds abort, grow and re-run
             pl.np = std::max<u64>(std::max<u64>(pl.np / 16, 1), np_floor_);
             pl.lg = 0;
@@ -1188,6 +1466,7 @@ private:
             const u64 per2 = (routed_max + G_ * pl.np - 1) / (G_ * pl.np);
             pl.cap = std::max<u64>(per2 / 4 + 1, cap_floor_);
             pl.layer_est = 0;
+            mark_cap_plan_ = std::max<u64>(per_owner / 8 + 1, mark_floor_);
         }
         pl.bloom_m = 0;
         if (cfg.dedup == DedupMode::bloom) {
@@ -1265,6 +1544,35 @@ private:
             cudaFree(s.b.stage);
             check(cudaMalloc(&s.b.stage, s.b.stage_cap * owner_slots<1>() * 8 * W), "owner staging");
             s.stage_words = W;
+        }
+        if (emit_) {
+            const u64 need = static_cast<u64>(G_) * mark_cap_plan_;
+            if (need > s.mark_alloc || !s.b.marks) {
+                const u64 cap = need + need / 4;
+                cudaFree(s.b.marks);
+                check(cudaMalloc(&s.b.marks, cap * 8), "marks");
+                s.mark_alloc = cap;
+                handles_dirty_ = true;
+            }
+            if (!s.b.mark_cnt) {
+                check(cudaMalloc(&s.b.mark_cnt, kMaxShards * 4), "mark counts");
+                handles_dirty_ = true;
+            }
+            s.b.mark_cap = mark_cap_plan_;
+            check(cudaMemsetAsync(s.b.mark_cnt, 0, kMaxShards * 4, stream_), "mark counts");
+            if (s.cmask_cap < s.b.layer_cap || !s.b.cmask) {
+                cudaFree(s.b.cmask);
+                check(cudaMalloc(&s.b.cmask, s.b.layer_cap * 16), "winner masks");
+                s.cmask_cap = s.b.layer_cap;
+            }
+            const u64 tiles_needed = count[s.me] / 2048 + 2;
+            if (tiles_needed > s.b.tile_cap) {
+                const u64 cap = std::max<u64>(tiles_needed * 2, u64{1} << 12);
+                cudaFree(s.b.tiles);
+                check(cudaMalloc(&s.b.tiles, cap * 8), "tiles");
+                check(cudaMemsetAsync(s.b.tiles, 0, cap * 8, stream_), "tiles");
+                s.b.tile_cap = cap;
+            }
         }
         if (pl.np + 1 > s.b.tile_cap || !s.b.tiles) {
             const u64 cap = std::max<u64>((pl.np + 1) * 2, u64{1} << 12);
@@ -1350,6 +1658,76 @@ private:
         ++launches_;
     }
 
+    void set_sources(Shard& s, const Plan& pl, int W) {
+        const u64 block = pl.np * pl.cap * (W + 1);
+        for (int src = 0; src < G_; ++src) {
+            if (!comm_) {
+                const Shard& from = local_[src];
+                s.b.src_recs[src] = from.b.out + s.me * block;
+                s.b.src_cnt[src] = from.b.out_cnt + s.me * pl.np;
+            } else if (src == s.me) {
+                s.b.src_recs[src] = s.b.out + s.me * block;
+                s.b.src_cnt[src] = s.b.out_cnt + s.me * pl.np;
+            } else if (p2p_) {
+                s.b.src_recs[src] = peer_out_[src] + s.me * block;
+                s.b.src_cnt[src] = peer_cnt_[src] + s.me * pl.np;
+            } else {
+                s.b.src_recs[src] = s.b.in + src * block;
+                s.b.src_cnt[src] = s.b.in_cnt + src * pl.np;
+            }
+        }
+    }
+
+    void launch_owner_emit(Shard& s, const Plan& pl, int W, bool bloom) {
+        Plan p = pl;
+        p.me = s.me;
+        set_sources(s, pl, W);
+        if (W == 1) {
+            if (bloom) k_owner_emit<1, true><<<grid_owner_[0], kOwnerThreads, owner_smem_bytes<1>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
+            else k_owner_emit<1, false><<<grid_owner_[0], kOwnerThreads, owner_smem_bytes<1>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
+        } else {
+            if (bloom) k_owner_emit<2, true><<<grid_owner_[1], kOwnerThreads, owner_smem_bytes<2>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
+            else k_owner_emit<2, false><<<grid_owner_[1], kOwnerThreads, owner_smem_bytes<2>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
+        }
+        check(cudaGetLastError(), "owner launch");
+        ++launches_;
+    }
+
+    // marks from every owner into this shard's winner masks, then its next layer
+    void launch_emit_append(Shard& s, const Plan& pl, int W) {
+        Plan p = pl;
+        p.me = s.me;
+        for (int o = 0; o < G_; ++o) {
+            if (!comm_) {  // virtual shards: the other shard's marks in place
+                s.b.src_marks[o] = local_[o].b.marks;
+                s.b.src_mark_cnt[o] = local_[o].b.mark_cnt;
+            } else if (o == s.me) {
+                s.b.src_marks[o] = s.b.marks;
+                s.b.src_mark_cnt[o] = s.b.mark_cnt;
+            } else {  // the owner's marks, read over NVLink
+                s.b.src_marks[o] = peer_marks_[o];
+                s.b.src_mark_cnt[o] = peer_mark_cnt_[o];
+            }
+        }
+        const int grid = grid_route_[0];
+        if (W == 1) {
+            k_apply_marks<1><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
+            k_emit_append<1><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
+        } else {
+            k_apply_marks<2><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
+            k_emit_append<2><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
+        }
+        check(cudaGetLastError(), "emit append launch");
+        launches_ += 2;
+    }
+
+    void route_barrier() {
+        Nccl& nc = Nccl::get();
+        Shard& s = local_[0];
+        nc.check(nc.AllGather(&s.d_ctl->mine, &s.d_ctl->all[0], sizeof(ShardStat), ncclUint8, comm_, stream_),
+                 "marks barrier");
+    }
+
     void launch_compact(Shard& s, const Plan& pl, int W) {
         Plan p = pl;
         p.me = s.me;
@@ -1410,8 +1788,8 @@ private:
     // bucket counts and maps its peers'. If any rank fails to map, all fall
     // back to the NCCL send/recv exchange.
     struct IpcRecord {
-        cudaIpcMemHandle_t out, cnt;
-        int ok, pad[3];
+        cudaIpcMemHandle_t out, cnt, marks, mark_cnt;
+        int ok, has_marks, pad[2];
     };
 
     void share_outboxes(Shard& s) {
@@ -1423,6 +1801,10 @@ private:
         IpcRecord mine{};
         mine.ok = cudaIpcGetMemHandle(&mine.out, s.b.out) == cudaSuccess &&
                   cudaIpcGetMemHandle(&mine.cnt, s.b.out_cnt) == cudaSuccess;
+        mine.has_marks = emit_ && s.b.marks && s.b.mark_cnt;
+        if (mine.has_marks)
+            mine.ok = mine.ok && cudaIpcGetMemHandle(&mine.marks, s.b.marks) == cudaSuccess &&
+                      cudaIpcGetMemHandle(&mine.mark_cnt, s.b.mark_cnt) == cudaSuccess;
         cudaGetLastError();
         check(cudaMemcpyAsync(d_handles_ + rec * s.me, &mine, rec, cudaMemcpyHostToDevice, stream_), "ipc h2d");
         nc.check(nc.AllGather(d_handles_ + rec * s.me, d_handles_, rec, ncclUint8, comm_, stream_), "ipc allgather");
@@ -1443,6 +1825,19 @@ private:
             }
             peer_out_[p] = static_cast<const u64*>(a);
             peer_cnt_[p] = static_cast<const unsigned*>(b);
+            if (h[p].has_marks) {
+                void* c = nullptr;
+                void* d = nullptr;
+                if (cudaIpcOpenMemHandle(&c, h[p].marks, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+                    cudaIpcOpenMemHandle(&d, h[p].mark_cnt, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    if (c) cudaIpcCloseMemHandle(c);
+                    ok = 0;
+                    break;
+                }
+                peer_marks_[p] = static_cast<const u64*>(c);
+                peer_mark_cnt_[p] = static_cast<const unsigned*>(d);
+            }
         }
         // agree: p2p only if every rank mapped every peer
         int* flags = reinterpret_cast<int*>(d_handles_);
@@ -1456,6 +1851,7 @@ private:
         if (!ok) {
             close_peers();
             p2p_ = false;
+            emit_ = false;  // emitter-stored layers need the NVLink pull
             s.b.box_cap = 0;  // reallocate with inboxes for the NCCL exchange
             s.b.cnt_cap = 0;
             std::fprintf(stderr, "[elimtw] CUDA IPC peer mapping unavailable: NCCL send/recv exchange\n");
@@ -1466,8 +1862,12 @@ private:
         for (int p = 0; p < kMaxShards; ++p) {
             if (peer_out_[p]) cudaIpcCloseMemHandle(const_cast<u64*>(peer_out_[p]));
             if (peer_cnt_[p]) cudaIpcCloseMemHandle(const_cast<unsigned*>(peer_cnt_[p]));
+            if (peer_marks_[p]) cudaIpcCloseMemHandle(const_cast<u64*>(peer_marks_[p]));
+            if (peer_mark_cnt_[p]) cudaIpcCloseMemHandle(const_cast<unsigned*>(peer_mark_cnt_[p]));
             peer_out_[p] = nullptr;
             peer_cnt_[p] = nullptr;
+            peer_marks_[p] = nullptr;
+            peer_mark_cnt_[p] = nullptr;
         }
     }
 
@@ -1568,6 +1968,12 @@ void shard_info(int* world, int* rank, int* virt) {
     ShardSet& s = ShardSet::instance();
     std::lock_guard<std::mutex> lock(s.mu);
     s.info(world, rank, virt);
+}
+
+void shard_set_mode(int emitter) {
+    ShardSet& s = ShardSet::instance();
+    std::lock_guard<std::mutex> lock(s.mu);
+    s.set_mode(emitter);
 }
 
 void shard_set_handoff(uint64_t states) {

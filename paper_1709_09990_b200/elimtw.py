@@ -124,6 +124,7 @@ def library() -> C.CDLL:
         "etwg_shard_info": (None, [_ip, _ip, _ip]),
         "etwg_shard_exchange_p2p": (C.c_int, []),
         "etwg_set_shard_handoff": (None, [C.c_uint64]),
+        "etwg_set_shard_mode": (None, [C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -486,6 +487,12 @@ def shard_init(uid: bytes, rank: int, world: int, device: int) -> None:
 def set_shard_handoff(states: int) -> None:
     """Layers up to `states` run replicated on every shard (0: shard from the root)."""
     library().etwg_set_shard_handoff(states)
+
+
+def set_shard_mode(mode: str) -> None:
+    """'emitter' (default): states stay on the shard that emitted them;
+    'owner': states move to their hash owner."""
+    library().etwg_set_shard_mode(1 if mode == "emitter" else 0)
 
 
 def shard_release() -> None:

@@ -20,13 +20,15 @@ pytestmark = pytest.mark.gpu
 def shards(E, gpu):
     """G virtual shards; by default sharded from the root (no replicated
     prefix) so every round exercises route / owner."""
-    def use(g, handoff=0):
+    def use(g, handoff=0, mode="emitter"):
         E.set_virtual_shards(g)
         E.set_shard_handoff(handoff)
+        E.set_shard_mode(mode)
         return g
     yield use
     E.set_virtual_shards(1)
     E.set_shard_handoff(1 << 19)
+    E.set_shard_mode("emitter")
 
 
 def _sets(run):
@@ -60,15 +62,18 @@ def _rows(name, rows):
     return elimtw.Graph.parse(instance_text(name)).rows()
 
 
+@pytest.mark.parametrize("mode", ["emitter", "owner"])
 @pytest.mark.parametrize("g,handoff", [(2, 0), (3, 0), (8, 0), (3, 2000), (8, 50000)])
-def test_sharded_exact_matches_single_device(E, shards, g, handoff):
+def test_sharded_exact_matches_single_device(E, shards, g, handoff, mode):
     """handoff > 0: the first layers run replicated on the single-device
-    engine, the first layer above `handoff` states is split by owner."""
+    engine, the first layer above `handoff` states is split between the
+    shards. mode: next-layer states stay on their emitting shard, or move to
+    their hash owner."""
     base = {}
     for name, rows, k in CASES:
         rows = _rows(name, rows)
         base[(name, k)] = E.decide(rows, k, dedup="exact")
-    shards(g, handoff)
+    shards(g, handoff, mode)
     for name, rows, k in CASES:
         rows = _rows(name, rows)
         got = E.decide(rows, k, dedup="exact")
@@ -92,12 +97,25 @@ def test_sharded_histories_are_min_rank_emissions(E, shards):
                 assert s >> v & 1, (r, hex(s), hex(h))
 
 
-def test_sharded_deterministic_for_fixed_g(E, shards):
+@pytest.mark.parametrize("mode", ["emitter", "owner"])
+def test_sharded_deterministic_for_fixed_g(E, shards, mode):
     rows = G.random_graph(2, 36, 0.3)
-    shards(4)
+    shards(4, mode=mode)
     a = E.decide(rows, 18, dedup="exact")
     b = E.decide(rows, 18, dedup="exact")
     assert a.layers == b.layers and (a.witness_set, a.witness_hist) == (b.witness_set, b.witness_hist)
+
+
+def test_emitter_and_owner_modes_agree(E, shards):
+    """Both placements of the next layer give the same counters and sets for
+    every shard count."""
+    rows = G.random_graph(1, 40, 0.3)
+    shards(4, mode="emitter")
+    emit = E.decide(rows, 21, dedup="exact")
+    shards(4, mode="owner")
+    own = E.decide(rows, 21, dedup="exact")
+    assert [x.tuple() for x in emit.rounds] == [x.tuple() for x in own.rounds]
+    assert _sets(emit) == _sets(own)
 
 
 def test_sharded_mmw_counters(E, shards):
@@ -174,7 +192,7 @@ def test_sharded_layers_live_on_their_owner(E, shards):
     consecutive states never decreases: every state sits on its owner."""
     from shard_model import owner_of
     rows = G.random_graph(1, 40, 0.3)
-    shards(3)
+    shards(3, mode="owner")
     run = E.decide(rows, 21, dedup="exact")
     for r, layer in enumerate(run.layers):
         owners = [owner_of(s, 3) for s, _ in layer]
@@ -212,6 +230,7 @@ sys.path.insert(0, ".")
 from paper_1709_09990_b200 import elimtw as E, generators as G
 E.set_virtual_shards(3)
 E.set_shard_handoff(int(sys.argv[1]))
+E.set_shard_mode(sys.argv[2])
 res = {}
 for name, rows, k, dedup, mmw in (("g", G.random_graph(1, 40, 0.3), 21, "exact", False),
                                   ("b", G.random_graph(2, 36, 0.3), 18, "bloom", False),
@@ -223,7 +242,7 @@ print(json.dumps(res))
 """
 
 
-def _tight_run(tight, handoff):
+def _tight_run(tight, handoff, mode="emitter"):
     import os
     import subprocess
     import sys
@@ -232,19 +251,20 @@ def _tight_run(tight, handoff):
     if tight:
         env["ETWG_SHARD_TIGHT"] = "1"
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-c", _TIGHT_CODE, str(handoff)], env=env, cwd=root,
+    out = subprocess.run([sys.executable, "-c", _TIGHT_CODE, str(handoff), mode], env=env, cwd=root,
                          capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
+@pytest.mark.parametrize("mode", ["emitter", "owner"])
 @pytest.mark.parametrize("handoff", [0, 3000])
-def test_sharded_rounds_survive_aborts(gpu, handoff):
+def test_sharded_rounds_survive_aborts(gpu, handoff, mode):
     """Undersized bucket, partition-table and layer plans (ETWG_SHARD_TIGHT)
     make sharded rounds abort on some shard, grow on every shard and re-run;
     the results equal the normally planned run."""
-    normal = _tight_run(False, handoff)
-    tight = _tight_run(True, handoff)
+    normal = _tight_run(False, handoff, mode)
+    tight = _tight_run(True, handoff, mode)
     assert tight["reruns"] > 0
     for key in ("g", "b", "m"):
         assert tight[key][0] == normal[key][0], key
