@@ -1,34 +1,42 @@
-// Owner-sharded wavefront across G devices: the multi-GPU
+// Sharded wavefront across G devices: the multi-GPU
 // replacement for the reference's decide / expand_layer (proj/src/dp.cpp:
-// 73-194), one shard per B200.
+// 73-194), one shard per B200 (or G virtual shards on one device, the
+// single-GPU double of the exchange).
 //
-// Every state S of a layer lives on its owner shard owner(S) =
-// mulhi(mix(S), G) (a hash independent of the partition hash and of the Bloom
-// probes). A round on every shard:
+// Every child S+v has an owner shard owner(S+v) = mulhi(mix(S+v), G) that
+// deduplicates it. A round on every shard:
 //
-//   k_route   K1 (candidates, graph.hpp:61-78 / dp.cpp:39-69) over the local
-//             parents; each child {S+v, rank, history} is appended to the
-//             outbox bucket (owner, partition) — partition = top bits of an
-//             independent hash, sized so one bucket's distinct keys fit a
-//             shared-memory table.
-//   exchange  outbox block d -> inbox slot `me` of shard d, with its bucket
-//             counts: NCCL grouped send/recv over NVLink (one process per
-//             GPU), or device copies between virtual shards of one device.
-//   k_owner   per partition, in partition order: exact dedup of the records
-//             every source sent (min emission rank per key, the history of
-//             the min-rank emission — dp.cpp:140-151 semantics), optional
-//             Bloom filter on the owner's slice (bloom.cpp:86-97), rank sort,
-//             ordered append to the local next layer (decoupled look-back).
-//   allgather per-shard counters (ncclAllGather / copies) — the per-level
-//             count reduction that decides termination (dp.cpp:176-188).
-//   k_finish  global stats, the capacity wall applied shard-major
-//             (emitted = min(unique, cap), dp.cpp:84-86, 152-155), next round.
+//   k_route     K1 (candidates, graph.hpp:61-78 / dp.cpp:39-69) over the
+//               local parents; each child record goes to the outbox bucket
+//               (owner, partition) — partition = top bits of an independent
+//               hash, sized so one bucket's distinct keys fit shared memory.
+//   exchange    owners read their buckets straight from the sources'
+//               outboxes: over NVLink through CUDA IPC mappings (a
+//               stream-ordered allgather is the barrier), or in place between
+//               virtual shards; fallback: NCCL grouped send/recv.
+//   emitter-stored layers (default):
+//     k_owner_emit   per partition: min emission rank per key (dp.cpp:140-151
+//                    semantics, emitters ranked cyclically from the owner so
+//                    every shard keeps its share), optional Bloom filter on
+//                    the owner's slice (bloom.cpp:86-97); one mark per winner
+//                    back to its emitter
+//     k_apply_marks  each shard ORs its marks into its parents' winner masks
+//     k_emit_append  ordered append of the marked children (rank order)
+//   owner-stored layers (ETWG_SHARD_MODE=owner, and the NCCL fallback):
+//     k_owner        per partition: min rank + history per key, rank sort,
+//                    survivors to staging; k_owner_compact builds the layer
+//   allgather   per-shard counters (ncclAllGather / copies) — the per-level
+//               count reduction that decides termination (dp.cpp:176-188).
+//   k_finish    global stats, the capacity wall applied shard-major
+//               (emitted = min(unique, cap), dp.cpp:84-86, 152-155).
 //
-// Exact-mode per-level sets and counters (expanded, emitted, duplicates,
-// mmw_pruned) equal the single-device engine's; layer order is
-// (partition, source shard, parent index, vertex), deterministic for a
-// given G. The host plans each round's bucket geometry from the previous
-// round's growth and re-runs a round whose buckets overflowed.
+// Layers of up to 2^19 states are expanded redundantly on every shard by the
+// single-device engine first (no communication); the first larger layer is
+// split between the shards. Exact-mode per-level sets and counters
+// (expanded, emitted, duplicates, mmw_pruned) equal the single-device
+// engine's; layer order is deterministic for a given G. The host plans each
+// round's bucket geometry from the previous round's growth and re-runs a
+// round whose buffers overflowed on any shard.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
