@@ -1807,12 +1807,16 @@ private:
         if (!d_handles_) check(cudaMalloc(&d_handles_, rec * kMaxShards + 64), "ipc handles");
         std::vector<IpcRecord> h(G_);
         IpcRecord mine{};
-        mine.ok = cudaIpcGetMemHandle(&mine.out, s.b.out) == cudaSuccess &&
-                  cudaIpcGetMemHandle(&mine.cnt, s.b.out_cnt) == cudaSuccess;
+        cudaError_t why = cudaSuccess;
+        auto ok_or = [&](cudaError_t e) {
+            if (e != cudaSuccess && why == cudaSuccess) why = e;
+            return e == cudaSuccess;
+        };
+        mine.ok = ok_or(cudaIpcGetMemHandle(&mine.out, s.b.out)) && ok_or(cudaIpcGetMemHandle(&mine.cnt, s.b.out_cnt));
         mine.has_marks = emit_ && s.b.marks && s.b.mark_cnt;
         if (mine.has_marks)
-            mine.ok = mine.ok && cudaIpcGetMemHandle(&mine.marks, s.b.marks) == cudaSuccess &&
-                      cudaIpcGetMemHandle(&mine.mark_cnt, s.b.mark_cnt) == cudaSuccess;
+            mine.ok = mine.ok && ok_or(cudaIpcGetMemHandle(&mine.marks, s.b.marks)) &&
+                      ok_or(cudaIpcGetMemHandle(&mine.mark_cnt, s.b.mark_cnt));
         cudaGetLastError();
         check(cudaMemcpyAsync(d_handles_ + rec * s.me, &mine, rec, cudaMemcpyHostToDevice, stream_), "ipc h2d");
         nc.check(nc.AllGather(d_handles_ + rec * s.me, d_handles_, rec, ncclUint8, comm_, stream_), "ipc allgather");
@@ -1820,12 +1824,17 @@ private:
         check(cudaStreamSynchronize(stream_), "ipc sync");
         int ok = 1;
         for (int p = 0; p < G_; ++p) ok &= h[p].ok;
+        if (trace_)
+            for (int p = 0; p < G_; ++p)
+                std::fprintf(stderr, "[shard %d] ipc record of %d: ok=%d marks=%d (mine ok=%d, %s)\n", s.me, p, h[p].ok,
+                             h[p].has_marks, mine.ok, cudaGetErrorString(why));
         for (int p = 0; ok && p < G_; ++p) {
             if (p == s.me) continue;
             void* a = nullptr;
             void* b = nullptr;
-            if (cudaIpcOpenMemHandle(&a, h[p].out, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-                cudaIpcOpenMemHandle(&b, h[p].cnt, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            if (trace_) std::fprintf(stderr, "[shard %d] opening peer %d handles\n", s.me, p);
+            if (!ok_or(cudaIpcOpenMemHandle(&a, h[p].out, cudaIpcMemLazyEnablePeerAccess)) ||
+                !ok_or(cudaIpcOpenMemHandle(&b, h[p].cnt, cudaIpcMemLazyEnablePeerAccess))) {
                 cudaGetLastError();
                 if (a) cudaIpcCloseMemHandle(a);
                 ok = 0;
@@ -1836,8 +1845,8 @@ private:
             if (h[p].has_marks) {
                 void* c = nullptr;
                 void* d = nullptr;
-                if (cudaIpcOpenMemHandle(&c, h[p].marks, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-                    cudaIpcOpenMemHandle(&d, h[p].mark_cnt, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                if (!ok_or(cudaIpcOpenMemHandle(&c, h[p].marks, cudaIpcMemLazyEnablePeerAccess)) ||
+                    !ok_or(cudaIpcOpenMemHandle(&d, h[p].mark_cnt, cudaIpcMemLazyEnablePeerAccess))) {
                     cudaGetLastError();
                     if (c) cudaIpcCloseMemHandle(c);
                     ok = 0;
@@ -1847,6 +1856,7 @@ private:
                 peer_mark_cnt_[p] = static_cast<const unsigned*>(d);
             }
         }
+        if (trace_) std::fprintf(stderr, "[shard %d] opened: ok=%d (%s)\n", s.me, ok, cudaGetErrorString(why));
         // agree: p2p only if every rank mapped every peer
         int* flags = reinterpret_cast<int*>(d_handles_);
         check(cudaMemcpyAsync(flags + s.me, &ok, sizeof(int), cudaMemcpyHostToDevice, stream_), "ipc flag");
@@ -1855,6 +1865,7 @@ private:
         check(cudaMemcpyAsync(all.data(), flags, sizeof(int) * G_, cudaMemcpyDeviceToHost, stream_), "ipc flag d2h");
         check(cudaStreamSynchronize(stream_), "ipc sync");
         for (int v : all) ok &= v;
+        if (trace_) std::fprintf(stderr, "[shard %d] flags %d %d -> ok=%d\n", s.me, all[0], G_ > 1 ? all[1] : -1, ok);
         handles_dirty_ = false;
         if (!ok) {
             close_peers();
@@ -1862,7 +1873,8 @@ private:
             emit_ = false;  // emitter-stored layers need the NVLink pull
             s.b.box_cap = 0;  // reallocate with inboxes for the NCCL exchange
             s.b.cnt_cap = 0;
-            std::fprintf(stderr, "[elimtw] CUDA IPC peer mapping unavailable: NCCL send/recv exchange\n");
+            std::fprintf(stderr, "[elimtw] CUDA IPC peer mapping unavailable (%s): NCCL send/recv exchange\n",
+                         why == cudaSuccess ? "a peer failed" : cudaGetErrorString(why));
         }
     }
 
