@@ -534,8 +534,11 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner_emit(const Params* __re
                     placed = smem_claim<W>(keys, h, key);
                     if (!placed) h = (h + 1) & (SLOTS - 1);
                 }
-                if (placed)
-                    atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), pri | packed);
+                if (placed) {
+                    const u64 mine = pri | packed;  // ranks only decrease: skip the atomic when already beaten
+                    if (!ETWG_CLAIM_PEEK || mine < *reinterpret_cast<volatile u64*>(ranks + h))
+                        atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), mine);
+                }
                 else
                     s_full = 1;
             }

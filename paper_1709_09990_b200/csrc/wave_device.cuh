@@ -527,8 +527,28 @@ __device__ __forceinline__ u64 child_rank(u64 parent_idx, int v) {
 
 // Shared-memory open-addressing claim: the slot at `keys + W*h` becomes
 // `key` if it was empty (0); true when the slot now holds `key`.
+#ifndef ETWG_CLAIM_PEEK
+#define ETWG_CLAIM_PEEK 1
+#endif
 template <int W>
 __device__ __forceinline__ bool smem_claim(u64* keys, unsigned h, const Set<W>& key) {
+#if ETWG_CLAIM_PEEK
+    // A slot only ever goes 0 -> key, so a plain read that shows a complete
+    // key is final: ours (claimed, no atomic) or another (probe on). Only an
+    // empty slot — or, at 128 bits, a read with a zero half, which may be a
+    // half-visible CAS (keys with an empty half always take this path) —
+    // takes the atomic.
+    if constexpr (W == 1) {
+        const u64 seen = *reinterpret_cast<volatile u64*>(keys + h);
+        if (seen) return seen == key.w[0];
+    } else {
+        u64 lo, hi;
+        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(lo), "=l"(hi)
+                     : "r"(static_cast<unsigned>(__cvta_generic_to_shared(keys + 2 * h))));
+        if (lo && hi) return lo == key.w[0] && hi == key.w[1];
+    }
+#endif
     if constexpr (W == 1) {
         const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(keys + h), 0ull, key.w[0]);
         return prev == 0 || prev == key.w[0];

@@ -130,6 +130,9 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_SCATTER_COMPACT
 #define ETWG_SCATTER_COMPACT false  // vertex-indexed boundary table (rank order keeps it L1-friendly)
 #endif
+#ifndef ETWG_PART_BATCH
+#define ETWG_PART_BATCH 4  // records loaded per thread before probing (k_exact_part)
+#endif
 #ifndef ETWG_PART_DIV
 #define ETWG_PART_DIV 3  // table slots per targeted distinct key
 #endif
@@ -357,46 +360,45 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
         __syncthreads();
         const unsigned cnt = B.cursors[part];
         const u64* recs = B.recs + part * cap * rec_words<W>();
-        for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
-            Set<W> key;
-            u64 rank;
-            if constexpr (W == 1) {
-                const ulonglong2 rec = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + i);
-                key.w[0] = rec.x;
-                rank = rec.y;
-            } else {
-                const ulonglong2 k2 = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + 2 * i);
-                const ulonglong2 r2 = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + 2 * i + 1);
-                key.w[0] = k2.x;
-                key.w[1] = k2.y;
-                rank = r2.x;
-            }
-            unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
-            bool placed = false;
-            for (int probe = 0; probe < 128 && !placed; ++probe) {
+        // PART_BATCH records in flight per thread before any probing: one
+        // outstanding 16 B load per thread cannot cover HBM latency at the
+        // 3 CTAs/SM the 64 KB tables allow
+        constexpr int kBatch = ETWG_PART_BATCH;
+        for (unsigned base = threadIdx.x; base < cnt; base += kBatch * blockDim.x) {
+            Set<W> keyv[kBatch];
+            u64 rankv[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const unsigned i = base + j * blockDim.x;
+                if (i >= cnt) break;
                 if constexpr (W == 1) {
-                    const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(keys + h), 0ull, key.w[0]);
-                    placed = prev == 0 || prev == key.w[0];
+                    const ulonglong2 rec = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + i);
+                    keyv[j].w[0] = rec.x;
+                    rankv[j] = rec.y;
                 } else {
-                    u64 lo, hi;
-                    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(keys + 2 * h));
-                    asm volatile(
-                        "{\n\t.reg .b128 c, s, d;\n\t"
-                        "mov.b128 c, {%2, %3};\n\t"
-                        "mov.b128 s, {%4, %5};\n\t"
-                        "atom.shared.cas.b128 d, [%6], c, s;\n\t"
-                        "mov.b128 {%0, %1}, d;\n\t}"
-                        : "=l"(lo), "=l"(hi)
-                        : "l"(0ull), "l"(0ull), "l"(key.w[0]), "l"(key.w[1]), "r"(sa)
-                        : "memory");
-                    placed = (lo | hi) == 0 || (lo == key.w[0] && hi == key.w[1]);
+                    const ulonglong2 k2 = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + 2 * i);
+                    const ulonglong2 r2 = __ldcs(reinterpret_cast<const ulonglong2*>(recs) + 2 * i + 1);
+                    keyv[j].w[0] = k2.x;
+                    keyv[j].w[1] = k2.y;
+                    rankv[j] = r2.x;
                 }
-                if (placed)
-                    atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), rank);
-                else
-                    h = (h + 1) & (SLOTS - 1);
             }
-            if (!placed) s_full = 1;
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                if (base + j * blockDim.x >= cnt) break;
+                const Set<W>& key = keyv[j];
+                const u64 rank = rankv[j];
+                unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
+                bool placed = false;
+                for (int probe = 0; probe < 128 && !placed; ++probe) {
+                    placed = smem_claim<W>(keys, h, key);
+                    if (!placed) h = (h + 1) & (SLOTS - 1);
+                }
+                // ranks only decrease: a slot already at or below ours needs no atomic
+                if (placed && (!ETWG_CLAIM_PEEK || rank < *reinterpret_cast<volatile u64*>(ranks + h)))
+                    atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), rank);
+                if (!placed) s_full = 1;
+            }
         }
         __syncthreads();
         if (s_full) {
