@@ -373,13 +373,7 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner(const Params* __restric
                     probe_start(h1, h2, pl.bloom_m, pos, step);
                     // distinct keys of one round meet the filter exactly once, so the
                     // reference's "any probed bit was clear" is the novelty test
-                    keep = false;
-                    for (int t = 1; t <= P->hashes; ++t) {
-                        const unsigned bit = 1u << (pos & 31);
-                        keep |= (atomicOr(B.bloom + (pos >> 5), bit) & bit) == 0;
-                        pos += step;
-                        if (pos >= pl.bloom_m) pos -= pl.bloom_m;
-                    }
+                    keep = bloom_or_probes(B.bloom, pl.bloom_m, pos, step, P->hashes);
                 }
                 if (keep) sortk[atomicAdd(&s_cnt, 1u)] = (rank << 12) | static_cast<u64>(i);
             }
@@ -566,14 +560,7 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner_emit(const Params* __re
                         const unsigned h2 = murmur_key<W>(key, kSeed2);
                         u64 pos, step;
                         probe_start(h1, h2, pl.bloom_m, pos, step);
-                        bool novel = false;
-                        for (int t = 1; t <= P->hashes; ++t) {
-                            const unsigned bit = 1u << (pos & 31);
-                            novel |= (atomicOr(B.bloom + (pos >> 5), bit) & bit) == 0;
-                            pos += step;
-                            if (pos >= pl.bloom_m) pos -= pl.bloom_m;
-                        }
-                        if (!novel) {
+                        if (!bloom_or_probes(B.bloom, pl.bloom_m, pos, step, P->hashes)) {
                             ranks[i] = ~u64{0};  // a false positive: dropped as the reference drops it
                             continue;
                         }

@@ -870,6 +870,34 @@ __device__ __forceinline__ bool bloom_set_bits(unsigned* bits, u64 m, u64 first,
     return any_clear;
 }
 
+// Sets the probe bits (h1 + i*h2) mod m, i = 1..hashes, of a key that meets
+// the filter once per round (bloom.cpp:86-97 on a distinct key); true when a
+// probed bit was clear. Eight atomics are in flight before any result is
+// used — consuming each return before the next probe (the plain loop) makes
+// every probe a dependent L2/HBM round trip on filters far larger than L2.
+__device__ __forceinline__ bool bloom_or_probes(unsigned* bits, u64 m, u64 first, u64 step, int hashes) {
+    constexpr int kInFlight = 8;
+    u64 pos = first;
+    bool clear = false;
+    for (int t = 0; t < hashes; t += kInFlight) {
+        unsigned word[kInFlight], bit[kInFlight];
+#pragma unroll
+        for (int j = 0; j < kInFlight; ++j) {
+            bit[j] = 0;
+            word[j] = 0;
+            if (t + j < hashes) {
+                bit[j] = 1u << (pos & 31);
+                word[j] = atomicOr(bits + (pos >> 5), bit[j]);
+                pos += step;
+                if (pos >= m) pos -= m;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kInFlight; ++j) clear |= bit[j] != 0 && (word[j] & bit[j]) == 0;
+    }
+    return clear;
+}
+
 // Tile status word: [epoch:24][flag:2][value:38]. The epoch changes with
 // every round attempt, so statuses left by earlier rounds read as "not yet
 // published" and the status array never needs clearing between rounds.

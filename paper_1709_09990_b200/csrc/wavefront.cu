@@ -422,14 +422,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
                 const unsigned h2 = murmur_key<W>(key, kSeed2);
                 u64 pos, step;
                 probe_start(h1, h2, m, pos, step);
-                bool novel = false;
-                for (int t = 1; t <= P->hashes; ++t) {
-                    const unsigned bit = 1u << (pos & 31);
-                    novel |= (atomicOr(bits + (pos >> 5), bit) & bit) == 0;
-                    pos += step;
-                    if (pos >= m) pos -= m;
-                }
-                if (!novel) continue;
+                if (!bloom_or_probes(bits, m, pos, step, P->hashes)) continue;
             }
             const u64 parent = rank / (64 * W);
             const int v = static_cast<int>(rank % (64 * W));
