@@ -130,6 +130,9 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_SCATTER_COMPACT
 #define ETWG_SCATTER_COMPACT false  // vertex-indexed boundary table (rank order keeps it L1-friendly)
 #endif
+#ifndef ETWG_EMIT_UNROLL
+#define ETWG_EMIT_UNROLL 2  // children emitted per lane per step in k_exact_scatter
+#endif
 #ifndef ETWG_PART_BATCH
 #define ETWG_PART_BATCH 4  // records loaded per thread before probing (k_exact_part)
 #endif
@@ -293,25 +296,38 @@ __global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __rest
         WarpFlat f;
         f.scan(M.count());
         bool full = false;
-        for (int t = 0; t < f.total; t += 32) {
-            const int j = t + lane;
-            const int src = f.source(j);
-            const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
-            const Set<W> Ms = shfl_set<W>(M, src);
-            const Set<W> Ss = shfl_set<W>(S, src);
-            if (j < f.total) {
-                const int v = nth_member<W>(Ms, j - excl);
-                Set<W> key = Ss;
-                key.add(v);
-                const u64 part = part_of<W>(key, pl.lg);
-                const unsigned slot = atomicAdd(B.cursors + part, 1u);
-                if (slot < pl.cap) {
-                    u64* rec = B.recs + (part * pl.cap + slot) * rec_words<W>();
+        // ETWG_EMIT_UNROLL children per lane per step: their bucket-cursor
+        // atomics are in flight together instead of one round trip each
+        constexpr int U = ETWG_EMIT_UNROLL;
+        for (int t = 0; t < f.total; t += 32 * U) {
+            Set<W> key[U];
+            u64 part[U], rank[U];
+            unsigned slot[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = t + 32 * u + lane;
+                const int src = f.source(j);
+                const int excl = __shfl_sync(kFull, f.incl, src) - __shfl_sync(kFull, f.cnt, src);
+                const Set<W> Ms = shfl_set<W>(M, src);
+                key[u] = shfl_set<W>(S, src);
+                slot[u] = ~0u;
+                if (j < f.total) {
+                    const int v = nth_member<W>(Ms, j - excl);
+                    key[u].add(v);
+                    part[u] = part_of<W>(key[u], pl.lg);
+                    rank[u] = child_rank<W>(base + src, v);
+                    slot[u] = atomicAdd(B.cursors + part[u], 1u);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (slot[u] == ~0u) continue;
+                if (slot[u] < pl.cap) {
+                    u64* rec = B.recs + (part[u] * pl.cap + slot[u]) * rec_words<W>();
                     if constexpr (W == 1) {
-                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(base + src, v));
+                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key[u].w[0], rank[u]);
                     } else {
-                        *reinterpret_cast<ulonglong4*>(rec) =
-                            make_ulonglong4(key.w[0], key.w[1], child_rank<W>(base + src, v), 0);
+                        *reinterpret_cast<ulonglong4*>(rec) = make_ulonglong4(key[u].w[0], key[u].w[1], rank[u], 0);
                     }
                 } else {
                     full = true;

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.txt 2>&1; tail -3 gpurun_out/gpu_tests.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
-timeout 600 python bench.py > gpurun_out/bench_v7.json 2> gpurun_out/bench_v7.err; tail -c 400 gpurun_out/bench_v7.json
+timeout 600 python tools/ab_lib.py alt_libs/libelimtw_base.so paper_1709_09990_b200/libelimtw.so 3 2>&1 | tail -4
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
