@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python tools/ab_lib.py alt_libs/libelimtw_base.so paper_1709_09990_b200/libelimtw.so 3 2>&1 | tail -4
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
+python tools/prof_decide.py 22 exact > gpurun_out/decide_stats_v8.txt 2>&1; head -2 gpurun_out/decide_stats_v8.txt
+for kern in k_exact_scatter k_exact_part k_append; do
+  timeout 900 python tools/ncu_top.py "$kern" ${kern}_v8 -- python tools/prof_decide.py 22 exact
+done
