@@ -130,6 +130,9 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_SCATTER_COMPACT
 #define ETWG_SCATTER_COMPACT false  // vertex-indexed boundary table (rank order keeps it L1-friendly)
 #endif
+#ifndef ETWG_APPEND_MINB
+#define ETWG_APPEND_MINB 4  // k_append: >= 4 resident CTAs per SM (registers <= 64)
+#endif
 #ifndef ETWG_EMIT_UNROLL
 #define ETWG_EMIT_UNROLL 2  // children emitted per lane per step in k_exact_scatter
 #endif
@@ -658,7 +661,7 @@ template <int W>
 constexpr int append_items() { return W == 1 ? 8 : 4; }
 
 template <int W>
-__global__ void __launch_bounds__(kThreads) k_append(const Params* __restrict__ P, Control* C,
+__global__ void __launch_bounds__(kThreads, ETWG_APPEND_MINB) k_append(const Params* __restrict__ P, Control* C,
                                                      Bufs B) {
     using BlockScan = cub::BlockScan<unsigned, kThreads>;
     constexpr int ITEMS = append_items<W>();
