@@ -140,7 +140,7 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #define ETWG_PART_BATCH 4  // records loaded per thread before probing (k_exact_part)
 #endif
 #ifndef ETWG_PART_DIV
-#define ETWG_PART_DIV 3  // table slots per targeted distinct key
+#define ETWG_PART_DIV 4  // table slots per targeted distinct key (3: +0.6 %, 5: +1.3 % per solve)
 #endif
 
 template <int W>

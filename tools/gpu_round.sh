@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.txt 2>&1; tail -3 gpurun_out/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
-timeout 600 python bench.py > gpurun_out/bench_v9.json 2> gpurun_out/bench_v9.err; tail -c 300 gpurun_out/bench_v9.json
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_v9.json 2> gpurun_out/bench_ref_v9.err; tail -c 300 gpurun_out/bench_ref_v9.json
+timeout 600 python bench.py > gpurun_out/bench_v10.json 2> gpurun_out/bench_v10.err; tail -c 200 gpurun_out/bench_v10.json
