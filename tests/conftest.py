@@ -53,3 +53,20 @@ def gpu(E):
 def instance_text(name):
     with open(os.path.join(HERE, "golden", "instances", name + ".gr")) as f:
         return f.read()
+
+
+@pytest.fixture(scope="session")
+def big_goldens():
+    """Reference outputs for the large configs (tests/golden/make_big_goldens.py)."""
+    with open(os.path.join(HERE, "golden", "big_goldens.json")) as f:
+        return json.load(f)
+
+
+def g48_golden():
+    """The reference's full G(48,0.2) sweep (cfg 4, the bench workload), or
+    None before tests/golden/make_big_goldens.py g48 has been run."""
+    path = os.path.join(HERE, "golden", "g48_ref.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)
