@@ -362,6 +362,97 @@ __device__ __forceinline__ Set<W> candidates_shared(const Set<W>* adj, int k, co
     return keep;
 }
 
+// K1 with the boundaries in registers (the degree test of expand_range,
+// dp.cpp:55-56, on Q(S,v) of graph.hpp:61-78). Q(S,v) = N(v)\S plus the
+// outside boundary B_K of every component K of G[S] that v touches, and v
+// touches K exactly when v is in B_K. So instead of a per-vertex table
+// R[u] = B_{K(u)} (64 entries per thread, local memory, read at a
+// different index by every lane of a warp), the components are kept as a
+// short list of boundaries:
+//   * a component whose boundary misses every eligible vertex is dropped;
+//   * one whose boundary has more than k+1 vertices rejects all of them
+//     (|Q(S,v)| >= |B_K| - 1 > k), one mask for all such components;
+//   * an isolated member u of S (boundary N(u)) goes into a mask and is
+//     read back from the shared adjacency rows;
+//   * every other component takes a register slot (kSlotRegs of them;
+//     further ones go to a local array walked with a loop-uniform index, so
+//     those loads stay coalesced). Measured on G(40,0.3) / G(48,0.2) layers:
+//     parents have 0-4 multi-vertex components, >4 in ~1 % of them.
+// The flood fill is one flat loop of exactly |S| pops (|S| is the round
+// number, the same for every lane), and the candidate loop runs over the
+// eligible set, whose size n - |S| - |forbidden| is also warp-uniform.
+#ifndef ETWG_K1
+#define ETWG_K1 2  // 2: register boundary slots; 1: per-vertex table (component_reach)
+#endif
+#ifndef ETWG_SLOT_REGS
+#define ETWG_SLOT_REGS 4
+#endif
+constexpr int kSlotRegs = ETWG_SLOT_REGS;
+
+template <int W>
+__device__ __forceinline__ bool single_member(const Set<W>& s) {
+    if constexpr (W == 1) {
+        return (s.w[0] & (s.w[0] - 1)) == 0;
+    } else {
+        return s.count() == 1;
+    }
+}
+
+template <int W>
+__device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, const Set<W>& S,
+                                                   const Set<W>& eligible) {
+    Set<W> slot[kSlotRegs];
+#pragma unroll
+    for (int j = 0; j < kSlotRegs; ++j) slot[j] = Set<W>::zero();
+    Set<W> spill[32 * W];  // multi-vertex components beyond the register slots
+    Set<W> sing = Set<W>::zero(), reject = Set<W>::zero();
+    int ns = 0;
+    Set<W> rem = S, frontier = Set<W>::zero(), comp = Set<W>::zero(), nb = Set<W>::zero();
+    const int r = S.count();
+    for (int it = 0; it < r; ++it) {
+        if (frontier.none()) {  // next component: seed from the unvisited members
+            frontier = Set<W>::bit(pop_any(rem));
+            comp = frontier;
+            nb = Set<W>::zero();
+        }
+        const Set<W> a = adj[pop_any(frontier)];
+        nb |= a;
+        const Set<W> fresh = a & rem;
+        rem = rem - fresh;
+        comp |= fresh;
+        frontier |= fresh;
+        if (frontier.any()) continue;
+        const Set<W> B = nb - S;  // the finished component's outside boundary
+        if ((B & eligible).none()) continue;
+        if (B.count() > k + 1) {
+            reject |= B;
+        } else if (single_member<W>(comp)) {
+            sing |= comp;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSlotRegs; ++j)
+                if (ns == j) slot[j] = B;
+            if (ns >= kSlotRegs) spill[ns - kSlotRegs] = B;
+            ++ns;
+        }
+    }
+    Set<W> keep = Set<W>::zero();
+    for_each_any(eligible - reject, [&](int v) {
+        const Set<W> a = adj[v];
+        Set<W> q = a - S;
+        if (q.count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
+        for_each_any(a & sing, [&](int u) { q |= adj[u]; });
+#pragma unroll
+        for (int j = 0; j < kSlotRegs; ++j)
+            if (slot[j].has(v)) q |= slot[j];
+        for (int j = kSlotRegs; j < ns; ++j)
+            if (spill[j - kSlotRegs].has(v)) q |= spill[j - kSlotRegs];
+        q.del(v);
+        if (q.count() <= k) keep.add(v);
+    });
+    return keep;
+}
+
 template <int W, bool MMW, bool COMPACT = false>
 __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, const Set<W>& S,
                                              const Set<W>& forbidden, u64& pruned, Set<W>* Rsh = nullptr) {
@@ -371,6 +462,7 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
     Set<W> keep = Set<W>::zero();
     if (eligible.none()) return keep;
     if constexpr (!MMW) {
+        if (ETWG_K1 == 2) return candidates_slots<W>(adj, k, S, eligible);
         if (Rsh && S.count() <= kShSlots) return candidates_shared<W>(adj, k, S, eligible, Rsh);
     }
     Set<W> R[N];

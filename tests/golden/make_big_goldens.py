@@ -9,13 +9,24 @@ built from /root/reference/proj/src by `make -C oracle ref`) through its own
         without MMW (acceptance criterion 4, proj/tests/acceptance.cpp:245-286).
         Runs in minutes here.
 
-    python tests/golden/make_big_goldens.py g48 [threads]
+    python tests/golden/make_big_goldens.py g48 THREADS K [K ...]
         G(48,0.2) seed 1 (cfg 4, the bench workload), exact dedup,
-        max_layer_states = 2^31, full k sweep. Its largest round holds ~1.8e9
-        child entries of 24 B in the reference's thread-local vectors plus the
-        concatenated copy (dp.cpp:118-135), which does not fit this container's
-        62 GB, so it runs on the GPU box's host (the prebuilt .so travels; the
-        reference tree is not read there). Output: tests/golden/g48_ref.json.
+        max_layer_states = 2^31: the reference's decide (dp.cpp:167-194) on
+        the attempts solve() makes (solver.cpp:21-67: the largest biconnected
+        block, the forbidden max clique, the improved graph per k), one JSON
+        per run: tests/golden/g48_ref_k<K..>.json with every round's
+        LayerStats and the outcome. The k = 24 attempt alone offers 9.4e9
+        children (1.86e9 in one round, 24 B each in the reference's
+        thread-local vectors plus the concatenated copy, dp.cpp:118-135): it
+        needs ~140 GB and ~30 min of the reference's single-threaded sorts, so
+        the sweep runs on the GPU box's host (16 cores, 196 GB) in pieces that
+        fit a call; the prebuilt .so travels, the reference tree is not read
+        there.
+
+    python tests/golden/make_big_goldens.py g48-merge
+        Merges the pieces and the cheap solve() prelude computed here (block,
+        clique, MMW bound, start k, improvement edges per k) into
+        tests/golden/g48_ref.json.
 
 The outputs are committed next to this script.
 """
@@ -73,23 +84,73 @@ def small() -> None:
     print("wrote", path)
 
 
-def g48(threads: int) -> None:
-    ref = RefLib()
+def _g48_block(ref):
     rows = G.random_graph(1, 48, 0.2)
-    t = time.time()
-    ex = ref.solve(rows, dedup="exact", threads=threads, cap=BIG_CAP, json_len=1 << 26)
-    wall = time.time() - t
-    tot = _totals(ex["stats"])
-    out = {"generated_by": "tests/golden/make_big_goldens.py g48 (reference elimtw via oracle/_ref)",
-           "graph": "random_graph(seed=1, n=48, p=0.2)", "options": {
-               "dedup": "exact", "max_layer_states": BIG_CAP, "threads": threads,
-               "emit_order": False},
-           "tw": ex["value"], "kind": ex["kind"], "exact_stats": ex["stats"],
-           "ref_wall_s": round(wall, 1), "host": _host(), "totals": tot}
-    path = os.path.join(HERE, "g48_ref.json")
-    with open(path, "w") as f:
-        json.dump(out, f, indent=1, sort_keys=True)
-    print("wrote", path, "tw", ex["value"], "wall", round(wall, 1), "s", tot)
+    blocks = ref.split(rows, 2)
+    verts = max(blocks, key=lambda b: len(b[0]))[0]
+    idx = {v: i for i, v in enumerate(verts)}
+    sub = []
+    for v in verts:
+        r = 0
+        for u in range(len(rows)):
+            if rows[v] >> u & 1 and u in idx:
+                r |= 1 << idx[u]
+        sub.append(r)
+    return rows, verts, sub
+
+
+def g48(threads: int, ks) -> None:
+    ref = RefLib()
+    _, _, sub = _g48_block(ref)
+    clique = ref.max_clique(sub)
+    out = {"generated_by": "tests/golden/make_big_goldens.py g48 (reference decide via oracle/_ref)",
+           "threads": threads, "host": _host(), "attempts": []}
+    for k in ks:
+        gk = ref.improve_graph(sub, k)
+        t = time.time()
+        run = ref.decide(gk, k, forbidden=clique, dedup="exact", cap=BIG_CAP, threads=threads,
+                         keep_layers=False)
+        dt = time.time() - t
+        out["attempts"].append({"k": k, "outcome": run.outcome, "overflowed": run.overflowed,
+                                "witness": run.witness_set, "ref_s": round(dt, 1),
+                                "layers": [[x.round, x.expanded, x.emitted, x.duplicates,
+                                            x.mmw_pruned, bool(x.overflowed)] for x in run.rounds]})
+        print("k", k, run.outcome, "expanded", sum(x.expanded for x in run.rounds), "s", round(dt, 1),
+              flush=True)
+        path = os.path.join(HERE, "g48_ref_k" + "_".join(map(str, ks)) + ".json")
+        with open(path, "w") as f:
+            json.dump(out, f, indent=1)
+
+
+def g48_merge() -> None:
+    ref = RefLib()
+    rows, verts, sub = _g48_block(ref)
+    clique = ref.max_clique(sub)
+    mmw = ref.mmw_lower_bound(sub)
+    start = max(bin(clique).count("1") - 1, mmw)
+    edges = sum(bin(r).count("1") for r in sub) // 2
+    attempts = {}
+    pieces = []
+    for name in sorted(os.listdir(HERE)):
+        if name.startswith("g48_ref_k") and name.endswith(".json"):
+            piece = json.load(open(os.path.join(HERE, name)))
+            pieces.append({"file": name, "threads": piece["threads"], "host": piece["host"]})
+            for a in piece["attempts"]:
+                gk = ref.improve_graph(sub, a["k"])
+                a["added_edges"] = sum(bin(r).count("1") for r in gk) // 2 - edges
+                attempts[a["k"]] = a
+    ks = sorted(attempts)
+    assert ks == list(range(start, ks[-1] + 1)), ks
+    assert all(attempts[k]["outcome"] == "infeasible" for k in ks[:-1])
+    assert attempts[ks[-1]]["outcome"] == "feasible"
+    out = {"generated_by": "tests/golden/make_big_goldens.py g48-merge (reference via oracle/_ref)",
+           "graph": "random_graph(seed=1, n=48, p=0.2)", "max_layer_states": BIG_CAP,
+           "block": verts, "clique_size": bin(clique).count("1"), "mmw_bound": mmw,
+           "start_k": start, "tw": ks[-1], "attempts": [attempts[k] for k in ks],
+           "expanded": sum(l[1] for k in ks for l in attempts[k]["layers"]), "pieces": pieces}
+    with open(os.path.join(HERE, "g48_ref.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("tw", out["tw"], "expanded", out["expanded"])
 
 
 if __name__ == "__main__":
@@ -97,6 +158,8 @@ if __name__ == "__main__":
     if what == "small":
         small()
     elif what == "g48":
-        g48(int(sys.argv[2]) if len(sys.argv) > 2 else (os.cpu_count() or 1))
+        g48(int(sys.argv[2]), [int(x) for x in sys.argv[3:]])
+    elif what == "g48-merge":
+        g48_merge()
     else:
         raise SystemExit(f"unknown target {what}")

@@ -6,7 +6,7 @@ import csv, os, re, subprocess, sys
 regex, name = sys.argv[1], sys.argv[2]
 cmd = sys.argv[sys.argv.index("--") + 1:]
 os.makedirs("gpurun_out", exist_ok=True)
-lst = f"gpurun_out/{name}_launches.csv"
+lst = f"{name}_launches.csv" if "/" in name else f"gpurun_out/{name}_launches.csv"
 subprocess.run(["ncu", "--metrics", "gpu__time_duration.sum", "--clock-control", "none", "-k",
                 f"regex:{regex}", "--csv", "--log-file", lst, *cmd], check=True,
                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
@@ -22,6 +22,6 @@ for r in rows[hdr + 1:]:
 best = max(range(len(times)), key=lambda i: times[i])
 print(f"{len(times)} launches of {regex}; longest #{best}: {times[best] / 1e3:.1f} us", flush=True)
 subprocess.run(["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "-k",
-                f"regex:{regex}", "-s", str(best), "-c", "1", "-f", "-o", f"gpurun_out/{name}", *cmd],
+                f"regex:{regex}", "-s", str(best), "-c", "1", "-f", "-o", name if "/" in name else f"gpurun_out/{name}", *cmd],
                check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
-print("captured", f"gpurun_out/{name}.ncu-rep")
+print("captured", name)
