@@ -283,7 +283,8 @@ def sharded_roofline(t, dev_ms, world):
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": None, "peak_source": peak_src, "per": "GPU",
             "nvlink_GBps_per_gpu": t["exchange_bytes"] / world / (dev_ms / 1e3) / 1e9,
-            "nvlink_peak_GBps": 770.0}
+            "nvlink_peak_GBps": 900.0,
+            "nvlink_peak_source": "NVLink 5, 900 GB/s per direction per GPU (SURVEY §8d)"}
 
 
 def bloom_probe(E, G):
@@ -433,6 +434,30 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def torchrun_argv(argv, gpus, port=None):
+    """The command that re-launches this bench as `gpus` ranks (one process
+    per GPU, torchrun, rendezvous on 127.0.0.1)."""
+    port = port or int(os.environ.get("MASTER_PORT", "29533"))
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def launch_ranks(args, argv):
+    """`bench.py --gpus N` outside torchrun: N > 1 needs N ranks, so re-exec
+    under torchrun; with fewer than N visible GPUs fail loudly instead of
+    reporting a 1-GPU number as N."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "error":
+                          f"--gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}"}),
+              flush=True)
+        raise SystemExit(2)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (ranks) on stderr
+    raise SystemExit(subprocess.call(torchrun_argv(argv, args.gpus), env=env))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -446,6 +471,13 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=4.0,
                     help="seconds of reference CPU work per --impl reference step")
     args = ap.parse_args()
+    _, world, _ = env_rank()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        launch_ranks(args, sys.argv[1:])
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -120,13 +120,15 @@ ELIMTW_API void etwg_set_shard_handoff(uint64_t states);
  * (env ETWG_SHARD_MODE=owner). The NCCL send/recv fallback always uses 0. */
 ELIMTW_API void etwg_set_shard_mode(int emitter);
 
-/* host preprocessing (no GPU needed); rows as above */
+/* host preprocessing (no GPU needed); rows as above. No exception crosses
+ * the ABI: the etw_status ones return ETW_ERROR_INVALID_ARGUMENT (NULL
+ * pointer, n outside 0..128) or ETW_ERROR_INTERNAL, the int ones -1. */
 ELIMTW_API void etwg_graph_rows(const etw_graph* g, uint64_t* rows);
-ELIMTW_API void etwg_max_clique(int n, const uint64_t* rows, uint64_t* out2);
-ELIMTW_API void etwg_disjoint_paths(int n, const uint64_t* rows, uint8_t* out);
-ELIMTW_API void etwg_improve_graph(int n, const uint64_t* rows, int k, uint64_t* out_rows);
+ELIMTW_API etw_status etwg_max_clique(int n, const uint64_t* rows, uint64_t* out2);
+ELIMTW_API etw_status etwg_disjoint_paths(int n, const uint64_t* rows, uint8_t* out);
+ELIMTW_API etw_status etwg_improve_graph(int n, const uint64_t* rows, int k, uint64_t* out_rows);
 ELIMTW_API int etwg_mmw_lower_bound(int n, const uint64_t* rows, const uint64_t* s, int cap);
-/* verts: concatenated original ids; returns block count */
+/* verts: concatenated original ids; returns block count (-1 on failure) */
 ELIMTW_API int etwg_split(int n, const uint64_t* rows, int mode, int* verts, int* sizes,
                           int* cuts);
 

@@ -528,40 +528,81 @@ void etwg_graph_rows(const etw_graph* g, uint64_t* rows) {
     }
 }
 
-void etwg_max_clique(int n, const uint64_t* rows, uint64_t* out2) {
-    HostSet c = max_clique(graph_from_words(n, rows));
-    out2[0] = c.w[0];
-    out2[1] = c.w[1];
+// Host preprocessing entry points: no exception crosses the ABI. The void
+// ones return ETW_OK / ETW_ERROR_INVALID_ARGUMENT / ETW_ERROR_INTERNAL, the
+// counting ones -1 on any failure (bad n, allocation failure).
+static etw_status prep_status(const std::exception_ptr& e) {
+    try {
+        std::rethrow_exception(e);
+    } catch (const std::invalid_argument&) {
+        return ETW_ERROR_INVALID_ARGUMENT;
+    } catch (...) {
+        return ETW_ERROR_INTERNAL;
+    }
 }
 
-void etwg_disjoint_paths(int n, const uint64_t* rows, uint8_t* out) {
-    PathCounts pc = disjoint_path_counts(graph_from_words(n, rows));
-    std::memcpy(out, pc.counts.data(), pc.counts.size());
+etw_status etwg_max_clique(int n, const uint64_t* rows, uint64_t* out2) {
+    if (!rows || !out2) return ETW_ERROR_INVALID_ARGUMENT;
+    try {
+        HostSet c = max_clique(graph_from_words(n, rows));
+        out2[0] = c.w[0];
+        out2[1] = c.w[1];
+        return ETW_OK;
+    } catch (...) {
+        return prep_status(std::current_exception());
+    }
 }
 
-void etwg_improve_graph(int n, const uint64_t* rows, int k, uint64_t* out_rows) {
-    Graph g = graph_from_words(n, rows);
-    Graph h = improve_graph(g, k, disjoint_path_counts(g));
-    for (int v = 0; v < n; ++v) {
-        out_rows[2 * v] = h.neighbors(v).w[0];
-        out_rows[2 * v + 1] = h.neighbors(v).w[1];
+etw_status etwg_disjoint_paths(int n, const uint64_t* rows, uint8_t* out) {
+    if (!rows || !out) return ETW_ERROR_INVALID_ARGUMENT;
+    try {
+        PathCounts pc = disjoint_path_counts(graph_from_words(n, rows));
+        std::memcpy(out, pc.counts.data(), pc.counts.size());
+        return ETW_OK;
+    } catch (...) {
+        return prep_status(std::current_exception());
+    }
+}
+
+etw_status etwg_improve_graph(int n, const uint64_t* rows, int k, uint64_t* out_rows) {
+    if (!rows || !out_rows) return ETW_ERROR_INVALID_ARGUMENT;
+    try {
+        Graph g = graph_from_words(n, rows);
+        Graph h = improve_graph(g, k, disjoint_path_counts(g));
+        for (int v = 0; v < n; ++v) {
+            out_rows[2 * v] = h.neighbors(v).w[0];
+            out_rows[2 * v + 1] = h.neighbors(v).w[1];
+        }
+        return ETW_OK;
+    } catch (...) {
+        return prep_status(std::current_exception());
     }
 }
 
 int etwg_mmw_lower_bound(int n, const uint64_t* rows, const uint64_t* s, int cap) {
-    return mmw_lower_bound(graph_from_words(n, rows), set_from_words(s), cap);
+    if (!rows || !s) return -1;
+    try {
+        return mmw_lower_bound(graph_from_words(n, rows), set_from_words(s), cap);
+    } catch (...) {
+        return -1;
+    }
 }
 
 int etwg_split(int n, const uint64_t* rows, int mode, int* verts, int* sizes, int* cuts) {
-    std::vector<SubInstance> subs =
-        split_instance(graph_from_words(n, rows), static_cast<SplitMode>(mode));
-    int off = 0;
-    for (size_t i = 0; i < subs.size(); ++i) {
-        sizes[i] = static_cast<int>(subs[i].to_original.size());
-        cuts[i] = subs[i].parent_cut;
-        for (int v : subs[i].to_original) verts[off++] = v;
+    if (!rows || !verts || !sizes || !cuts) return -1;
+    try {
+        std::vector<SubInstance> subs =
+            split_instance(graph_from_words(n, rows), static_cast<SplitMode>(mode));
+        int off = 0;
+        for (size_t i = 0; i < subs.size(); ++i) {
+            sizes[i] = static_cast<int>(subs[i].to_original.size());
+            cuts[i] = subs[i].parent_cut;
+            for (int v : subs[i].to_original) verts[off++] = v;
+        }
+        return static_cast<int>(subs.size());
+    } catch (...) {
+        return -1;
     }
-    return static_cast<int>(subs.size());
 }
 
 }  // extern "C"

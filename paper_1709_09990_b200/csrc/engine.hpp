@@ -87,6 +87,7 @@ DecideResult device_decide_prefix(const Graph& g, int k, const HostSet& forbidde
                                   EngineLayer& handoff);
 int engine_device();  // the single-device engine's CUDA device (-1 without one)
 void engine_release_buffers();  // frees the single-device engine's round buffers
+void engine_bind_device(int dev);  // (re)binds the single-device engine to CUDA device dev
 
 struct ExpandResult {
     std::vector<State> states;

@@ -71,6 +71,9 @@ constexpr int kMaxShards = 8;
 #endif
 constexpr int kOwnerThreads = 512;
 constexpr int kRouteThreads = 256;
+// parents per look-back tile of k_emit_append (its ITEMS x kRouteThreads);
+// the host sizes the tile-status array from the same figure
+constexpr unsigned long long emit_span(int W) { return static_cast<unsigned long long>(kRouteThreads) * (W == 1 ? 8 : 4); }
 
 template <int W>
 constexpr int owner_slots() { return 2048; }
@@ -612,6 +615,7 @@ __global__ void __launch_bounds__(kRouteThreads) k_emit_append(ShardCtl* C, Shar
     using BlockScan = cub::BlockScan<unsigned, kRouteThreads>;
     constexpr int ITEMS = W == 1 ? 8 : 4;
     constexpr u64 kSpan = static_cast<u64>(kRouteThreads) * ITEMS;
+    static_assert(kSpan == emit_span(W), "host tile sizing");
     __shared__ typename BlockScan::TempStorage scan_tmp;
     __shared__ u64 s_prefix, s_tile;
     if (C->stop) return;
@@ -891,6 +895,7 @@ public:
         release();
         Nccl& nc = Nccl::get();
         engine_release_buffers();
+        engine_bind_device(device);  // the replicated prefix runs on the shard's GPU too
         init_device(device);
         ncclUniqueId uid;
         std::memcpy(&uid, id, sizeof uid);
@@ -1563,7 +1568,7 @@ private:
                 check(cudaMalloc(&s.b.cmask, s.b.layer_cap * 16), "winner masks");
                 s.cmask_cap = s.b.layer_cap;
             }
-            const u64 tiles_needed = count[s.me] / 2048 + 2;
+            const u64 tiles_needed = (count[s.me] + emit_span(W) - 1) / emit_span(W) + 2;
             if (tiles_needed > s.b.tile_cap) {
                 const u64 cap = std::max<u64>(tiles_needed * 2, u64{1} << 12);
                 cudaFree(s.b.tiles);

@@ -931,6 +931,7 @@ public:
 
 private:
     int init_state_ = 0;  // 0 unknown, 1 ok, 2 no device
+    int bound_device_ = -1;  // set by bind_device (shard init); else ETWG_DEVICE or 0
     DeviceInfo info_;
     cudaStream_t stream_ = nullptr;
     Params* d_params_ = nullptr;
@@ -972,6 +973,39 @@ private:
         if (kind == cudaMemcpyDeviceToHost) prof.t.d2h_bytes += bytes;
     }
 
+public:
+    // Moves the engine to device `dev` (a shard's device: one process per
+    // GPU under torchrun). Before first use it only records the choice;
+    // afterwards the engine is torn down and re-initialised there on next use.
+    void bind_device(int dev) {
+        if (init_state_ == 1 && info_.device == dev) return;
+        if (init_state_ == 1) teardown();
+        bound_device_ = dev;
+        init_state_ = 0;
+    }
+
+    void teardown() {
+        release_buffers();
+        cudaSetDevice(info_.device);
+        cudaStreamDestroy(stream_);
+        cudaFree(d_params_);
+        cudaFreeHost(h_params_);
+        cudaFree(d_ctl_);
+        cudaFreeHost(h_ctl_);
+        cudaFree(b_.locks);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(ev_[i]);
+            cudaEventDestroy(tev_[i]);
+            ev_[i] = tev_[i] = nullptr;
+        }
+        stream_ = nullptr;
+        d_params_ = h_params_ = nullptr;
+        d_ctl_ = h_ctl_ = nullptr;
+        b_.locks = nullptr;
+        init_state_ = 0;
+    }
+
+private:
     void init() {
         int count = 0;
         if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -981,6 +1015,7 @@ private:
         }
         int dev = 0;
         if (const char* e = std::getenv("ETWG_DEVICE")) dev = std::atoi(e);
+        if (bound_device_ >= 0) dev = bound_device_;
         check(cudaSetDevice(dev), "cudaSetDevice");
         cudaDeviceProp prop;
         check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
@@ -1290,6 +1325,14 @@ private:
         for (;;) {
             const int start = static_cast<int>(h_ctl_->round);
             const int end = std::min(rounds, start + chunk);
+            if (epoch_ + static_cast<unsigned>(end - start) + 1 >= kEpochMask) {
+                // the device advances the epoch once per round and would wrap
+                // inside this chunk: restart the tags from a cleared state now
+                epoch_ = 1;
+                clear_tagged();
+                h_ctl_->epoch = epoch_;
+                copy(&d_ctl_->epoch, &h_ctl_->epoch, sizeof(unsigned), cudaMemcpyHostToDevice, "epoch reset");
+            }
             for (int r = start; r < end; ++r) {
                 if (W == 1) launch_round<1>(cfg);
                 else launch_round<2>(cfg);
@@ -1463,6 +1506,12 @@ void engine_release_buffers() {
     Engine& e = Engine::instance();
     std::lock_guard<std::mutex> lock(e.mu);
     e.release_buffers();
+}
+
+void engine_bind_device(int dev) {
+    Engine& e = Engine::instance();
+    std::lock_guard<std::mutex> lock(e.mu);
+    e.bind_device(dev);
 }
 
 int engine_device() {

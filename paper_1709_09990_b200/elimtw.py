@@ -112,9 +112,9 @@ def library() -> C.CDLL:
         "etwg_timer_begin": (None, []),
         "etwg_timer_end": (C.c_double, []),
         "etwg_graph_rows": (None, [vp, _u64p]),
-        "etwg_max_clique": (None, [C.c_int, _u64p, _u64p]),
-        "etwg_disjoint_paths": (None, [C.c_int, _u64p, _u8p]),
-        "etwg_improve_graph": (None, [C.c_int, _u64p, C.c_int, _u64p]),
+        "etwg_max_clique": (C.c_int, [C.c_int, _u64p, _u64p]),
+        "etwg_disjoint_paths": (C.c_int, [C.c_int, _u64p, _u8p]),
+        "etwg_improve_graph": (C.c_int, [C.c_int, _u64p, C.c_int, _u64p]),
         "etwg_mmw_lower_bound": (C.c_int, [C.c_int, _u64p, _u64p, C.c_int]),
         "etwg_split": (C.c_int, [C.c_int, _u64p, C.c_int, _ip, _ip, _ip]),
         "etwg_set_virtual_shards": (C.c_int, [C.c_int, C.c_char_p, C.c_size_t]),
@@ -508,28 +508,38 @@ def shard_info() -> dict:
 
 # host preprocessing (no device needed)
 
+def _prep(status: int, what: str) -> None:
+    if status == ETW_ERROR_INVALID_ARGUMENT:
+        raise ValueError(f"{what}: invalid argument")
+    if status != ETW_OK:
+        raise ElimtwError(f"{what}: internal error")
+
+
 def max_clique(rows: Sequence[int]) -> int:
     out = (C.c_uint64 * 2)()
-    library().etwg_max_clique(len(rows), _words(rows), out)
+    _prep(library().etwg_max_clique(len(rows), _words(rows), out), "max_clique")
     return out[0] | (out[1] << 64)
 
 
 def disjoint_paths(rows: Sequence[int]) -> List[int]:
     n = len(rows)
     out = (C.c_uint8 * max(1, n * n))()
-    library().etwg_disjoint_paths(n, _words(rows), out)
+    _prep(library().etwg_disjoint_paths(n, _words(rows), out), "disjoint_paths")
     return list(out[: n * n])
 
 
 def improve_graph(rows: Sequence[int], k: int) -> List[int]:
     n = len(rows)
     out = (C.c_uint64 * max(2, 2 * n))()
-    library().etwg_improve_graph(n, _words(rows), k, out)
+    _prep(library().etwg_improve_graph(n, _words(rows), k, out), "improve_graph")
     return [out[2 * v] | (out[2 * v + 1] << 64) for v in range(n)]
 
 
 def mmw_lower_bound(rows: Sequence[int], s: int = 0, cap: int = 1 << 30) -> int:
-    return library().etwg_mmw_lower_bound(len(rows), _words(rows), _set_words(s), cap)
+    b = library().etwg_mmw_lower_bound(len(rows), _words(rows), _set_words(s), cap)
+    if b < 0:
+        raise ValueError("mmw_lower_bound: invalid graph")
+    return b
 
 
 def split(rows: Sequence[int], mode: str = "biconnected"):
@@ -538,6 +548,8 @@ def split(rows: Sequence[int], mode: str = "biconnected"):
     sizes = (C.c_int * (n + 2))()
     cuts = (C.c_int * (n + 2))()
     m = library().etwg_split(n, _words(rows), SPLIT[mode], verts, sizes, cuts)
+    if m < 0:
+        raise ValueError("split: invalid graph")
     out, off = [], 0
     for i in range(m):
         out.append((list(verts[off: off + sizes[i]]), cuts[i]))

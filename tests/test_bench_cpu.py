@@ -48,3 +48,30 @@ def test_reference_arm_line(ref):
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_gpus_flag_relaunches_under_torchrun(bench):
+    """`bench.py --gpus N` outside torchrun re-launches itself as N ranks on
+    127.0.0.1 (one process per GPU)."""
+    argv = bench.torchrun_argv(["--gpus", "4", "--steps", "2"], 4, port=29999)
+    assert argv[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in argv and "--master-addr=127.0.0.1" in argv
+    assert argv[-4:] == ["--gpus", "4", "--steps", "2"] and argv[-5].endswith("bench.py")
+
+
+def test_gpus_flag_fails_loudly_without_enough_devices():
+    """No silent N=1 number for --gpus 2: with fewer visible GPUs the bench
+    exits non-zero and says why (this container has none)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2"],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 2
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and "needs 2 visible CUDA devices" in line["error"]
+
+
+def test_world_mismatch_is_an_error():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2"],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode != 0 and "WORLD_SIZE=1" in p.stderr

@@ -128,17 +128,38 @@ def test_sharded_mmw_counters(E, shards):
 
 
 def test_sharded_capacity_wall(E, shards):
-    """Truncation keeps min(unique, cap) states (dp.cpp:152-155) shard-major."""
+    """Truncation keeps min(unique, cap) states (dp.cpp:152-155), but
+    shard-major, not the reference's lowest global emission ranks: sharded
+    layers have no global rank order. So the sharded run matches the
+    single-device run (counters AND sets) up to and including the counters
+    of the first overflowed round; from its kept SET on, the runs may
+    diverge (documented in DESIGN.md §7: sharded parity excludes
+    overflowed decides; single-device truncation is reference-exact)."""
     rows = G.random_graph(1, 40, 0.3)
     want = E.decide(rows, 22, dedup="exact", cap=20_000)
     shards(4)
     got = E.decide(rows, 22, dedup="exact", cap=20_000)
-    assert [x.emitted for x in got.rounds[:6]] == [x.emitted for x in want.rounds[:6]]
+    first = next(i for i, x in enumerate(want.rounds) if x.overflowed)
+    assert first > 0
+    assert _counters(got)[: first + 1] == _counters(want)[: first + 1]
+    assert _sets(got)[:first] == _sets(want)[:first]
+    assert got.rounds[first].emitted == want.rounds[first].emitted == 20_000
     assert got.overflowed == want.overflowed
-    for (a, b) in zip(got.rounds, want.rounds):
-        if not b.overflowed:
-            continue
-        assert a.emitted == b.emitted == 20_000
+    for a in got.rounds:
+        assert a.emitted <= 20_000
+
+
+def test_sharded_128bit_large_shard_layers(E, shards):
+    """W = 2 emitter-stored layers above 4.2M states per shard (the minimum
+    tile-status array covers 4096 tiles of 1024 parents at W = 2): counters
+    equal the single-device engine's."""
+    rows = G.random_graph(3, 70, 0.5)
+    want = E.decide(rows, 60, dedup="exact", rounds=4, cap=1 << 31, keep_layers=False)
+    assert want.rounds[-1].emitted > 2 * 4096 * 1024
+    shards(2)
+    got = E.decide(rows, 60, dedup="exact", rounds=4, cap=1 << 31, keep_layers=False)
+    assert _counters(got) == _counters(want)
+    assert got.outcome == want.outcome
 
 
 def test_sharded_bloom_subset_of_exact(E, shards):

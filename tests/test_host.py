@@ -181,3 +181,19 @@ def test_shard_api_validates_arguments_without_a_device(E):
     E.set_virtual_shards(1)  # "off" is always accepted
     assert D.init_shards() == E.shard_info()  # world 1 (no torchrun env): a no-op
     assert E.shard_info()["world"] == 1
+
+
+def test_preprocess_errors_do_not_cross_the_abi(E):
+    """etwg_* preprocessing entry points map exceptions to status codes
+    (graph_from_words rejects n > 128) instead of terminating the process."""
+    lib = E.library()
+    rows = (ctypes.c_uint64 * 512)()
+    out = (ctypes.c_uint64 * 512)()
+    assert lib.etwg_max_clique(200, rows, out) == E.ETW_ERROR_INVALID_ARGUMENT
+    assert lib.etwg_improve_graph(-1, rows, 3, out) == E.ETW_ERROR_INVALID_ARGUMENT
+    assert lib.etwg_max_clique(3, None, out) == E.ETW_ERROR_INVALID_ARGUMENT
+    assert lib.etwg_mmw_lower_bound(200, rows, out, 5) == -1
+    v = (ctypes.c_int * 4)()
+    assert lib.etwg_split(200, rows, 2, v, v, v) == -1
+    with pytest.raises(ValueError):
+        E.max_clique([0] * 200)
