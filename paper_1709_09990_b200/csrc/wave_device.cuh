@@ -399,58 +399,96 @@ __device__ __forceinline__ bool single_member(const Set<W>& s) {
 }
 
 template <int W>
-__device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, const Set<W>& S,
-                                                   const Set<W>& eligible) {
-    Set<W> slot[kSlotRegs];
+struct Comps {
+    Set<W> slot[kSlotRegs];  // constant-index access only: stays in registers
+    Set<W> sing, reject;
+    int ns;
+    // multi-vertex components beyond the register slots live in a separate
+    // local array (kept out of the struct so the struct stays in registers)
+    using Spill = Set<W>[32 * W];
+
+    // The components of G[S] whose boundary meets `targets`; a boundary of
+    // more than `reject_above` vertices goes to `reject` instead of a slot.
+    __device__ __forceinline__ void build(const Set<W>* adj, const Set<W>& S, const Set<W>& targets,
+                                          int reject_above, Spill& spill) {
 #pragma unroll
-    for (int j = 0; j < kSlotRegs; ++j) slot[j] = Set<W>::zero();
-    Set<W> spill[32 * W];  // multi-vertex components beyond the register slots
-    Set<W> sing = Set<W>::zero(), reject = Set<W>::zero();
-    int ns = 0;
-    Set<W> rem = S, frontier = Set<W>::zero(), comp = Set<W>::zero(), nb = Set<W>::zero();
-    const int r = S.count();
-    for (int it = 0; it < r; ++it) {
-        if (frontier.none()) {  // next component: seed from the unvisited members
-            frontier = Set<W>::bit(pop_any(rem));
-            comp = frontier;
-            nb = Set<W>::zero();
-        }
-        const Set<W> a = adj[pop_any(frontier)];
-        nb |= a;
-        const Set<W> fresh = a & rem;
-        rem = rem - fresh;
-        comp |= fresh;
-        frontier |= fresh;
-        if (frontier.any()) continue;
-        const Set<W> B = nb - S;  // the finished component's outside boundary
-        if ((B & eligible).none()) continue;
-        if (B.count() > k + 1) {
-            reject |= B;
-        } else if (single_member<W>(comp)) {
-            sing |= comp;
-        } else {
+        for (int j = 0; j < kSlotRegs; ++j) slot[j] = Set<W>::zero();
+        sing = reject = Set<W>::zero();
+        ns = 0;
+        Set<W> rem = S, frontier = Set<W>::zero(), comp = Set<W>::zero(), nb = Set<W>::zero();
+        const int r = S.count();
+        for (int it = 0; it < r; ++it) {
+            if (frontier.none()) {  // next component: seed from the unvisited members
+                frontier = Set<W>::bit(pop_any(rem));
+                comp = frontier;
+                nb = Set<W>::zero();
+            }
+            const Set<W> a = adj[pop_any(frontier)];
+            nb |= a;
+            const Set<W> fresh = a & rem;
+            rem = rem - fresh;
+            comp |= fresh;
+            frontier |= fresh;
+            if (frontier.any()) continue;
+            const Set<W> B = nb - S;  // the finished component's outside boundary
+            if ((B & targets).none()) continue;
+            if (B.count() > reject_above) {
+                reject |= B;
+            } else if (single_member<W>(comp)) {
+                sing |= comp;
+            } else {
 #pragma unroll
-            for (int j = 0; j < kSlotRegs; ++j)
-                if (ns == j) slot[j] = B;
-            if (ns >= kSlotRegs) spill[ns - kSlotRegs] = B;
-            ++ns;
+                for (int j = 0; j < kSlotRegs; ++j)
+                    if (ns == j) slot[j] = B;
+                if (ns >= kSlotRegs) spill[ns - kSlotRegs] = B;
+                ++ns;
+            }
         }
     }
-    Set<W> keep = Set<W>::zero();
-    for_each_any(eligible - reject, [&](int v) {
-        const Set<W> a = adj[v];
-        Set<W> q = a - S;
-        if (q.count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
-        for_each_any(a & sing, [&](int u) { q |= adj[u]; });
+
+    // Q(S,v) \ {v} from its first term N(v) \ S = a - S (exact for v in
+    // `targets` outside `reject`)
+    __device__ __forceinline__ Set<W> q(const Set<W>* adj, const Set<W>& a, Set<W> q0, int v,
+                                        const Spill& spill) const {
+        for_each_any(a & sing, [&](int u) { q0 |= adj[u]; });
 #pragma unroll
         for (int j = 0; j < kSlotRegs; ++j)
-            if (slot[j].has(v)) q |= slot[j];
+            if (slot[j].has(v)) q0 |= slot[j];
         for (int j = kSlotRegs; j < ns; ++j)
-            if (spill[j - kSlotRegs].has(v)) q |= spill[j - kSlotRegs];
-        q.del(v);
-        if (q.count() <= k) keep.add(v);
+            if (spill[j - kSlotRegs].has(v)) q0 |= spill[j - kSlotRegs];
+        q0.del(v);
+        return q0;
+    }
+
+    __device__ __forceinline__ Set<W> q(const Set<W>* adj, const Set<W>& S, int v, const Spill& spill) const {
+        const Set<W> a = adj[v];
+        return q(adj, a, a - S, v, spill);
+    }
+};
+
+template <int W>
+__device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, const Set<W>& S,
+                                                   const Set<W>& eligible) {
+    Comps<W> c;
+    typename Comps<W>::Spill spill;
+    c.build(adj, S, eligible, k + 1, spill);  // |Q(S,v)| >= |B_K| - 1 for v in B_K
+    Set<W> keep = Set<W>::zero();
+    for_each_any(eligible - c.reject, [&](int v) {
+        const Set<W> a = adj[v];
+        const Set<W> q0 = a - S;
+        if (q0.count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
+        if (c.q(adj, a, q0, v, spill).count() <= k) keep.add(v);
     });
     return keep;
+}
+
+// Q(S,w) for every open w (the minor-min-width input, dp.cpp:51-53)
+template <int W>
+__device__ __forceinline__ void q_rows(const Set<W>* adj, const Set<W>& S, const Set<W>& open, Set<W>* rows) {
+    Comps<W> c;
+    typename Comps<W>::Spill spill;
+    c.build(adj, S, open, 1 << 30, spill);
+    for_each_any(open, [&](int w) { rows[w] = c.q(adj, S, w, spill); });
 }
 
 template <int W, bool MMW, bool COMPACT = false>
@@ -466,7 +504,7 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
         if (Rsh && S.count() <= kShSlots) return candidates_shared<W>(adj, k, S, eligible, Rsh);
     }
     Set<W> R[N];
-    component_reach<W, COMPACT>(adj, S, R);
+    if (ETWG_K1 != 2) component_reach<W, COMPACT>(adj, S, R);
     if constexpr (!MMW) {
         for_each_any(eligible, [&](int v) {
             if ((adj[v] - S).count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
@@ -474,7 +512,10 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
         });
     } else {
         Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
-        for (int w : members(open)) rows[w] = reach_from<W, COMPACT>(adj, S, R, w);
+        if (ETWG_K1 == 2)
+            q_rows<W>(adj, S, open, rows);
+        else
+            for (int w : members(open)) rows[w] = reach_from<W, COMPACT>(adj, S, R, w);
         for (int v : members(eligible)) {
             if (rows[v].count() > k) continue;
             if (mmw_child<W>(n, k, S, v, rows) > k) {
@@ -519,9 +560,14 @@ __device__ __forceinline__ Set<W> warp_candidates(const Set<W>* adj, int n, int 
             const Set<W> Ss = shfl_set<W>(S, src);
             if (j < f.total) {
                 const int v = nth_member<W>(Ms, j - excl);
-                Set<W> R[N], rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
-                component_reach<W, COMPACT>(adj, Ss, R);
-                for (int w : members(Set<W>::prefix(n) - Ss)) rows[w] = reach_from<W, COMPACT>(adj, Ss, R, w);
+                Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
+                if (ETWG_K1 == 2) {
+                    q_rows<W>(adj, Ss, Set<W>::prefix(n) - Ss, rows);
+                } else {
+                    Set<W> R[N];
+                    component_reach<W, COMPACT>(adj, Ss, R);
+                    for (int w : members(Set<W>::prefix(n) - Ss)) rows[w] = reach_from<W, COMPACT>(adj, Ss, R, w);
+                }
                 if (mmw_child<W>(n, k, Ss, v, rows) > k)
                     ++pruned;
                 else
@@ -553,21 +599,38 @@ __device__ __forceinline__ Set<W> warp_parent_candidates(const Set<W>* adj, int 
     const Set<W> open = Set<W>::prefix(n) - S;
     const Set<W> eligible = open - forbidden;
     if (eligible.none()) return Set<W>::zero();
+#if ETWG_K1 == 2
+    // S is warp-uniform: every lane builds the same component list (no
+    // serial lane-0 fill, no shared table)
+    Comps<W> c;
+    typename Comps<W>::Spill spill;
+    c.build(adj, S, MMW ? open : eligible, MMW ? (1 << 30) : k + 1, spill);
+#else
     if (lane == 0) component_reach<W, false>(adj, S, R);
     __syncwarp();
+#endif
     Set<W> mine = Set<W>::zero();
     if constexpr (!MMW) {
         const int ne = eligible.count();
         for (int i = lane; i < ne; i += 32) {
             const int v = nth_member<W>(eligible, i);
-            if ((adj[v] - S).count() > k) continue;
+            const Set<W> q0 = adj[v] - S;
+            if (q0.count() > k) continue;
+#if ETWG_K1 == 2
+            if (!c.reject.has(v) && c.q(adj, adj[v], q0, v, spill).count() <= k) mine.add(v);
+#else
             if (reach_from<W, false>(adj, S, R, v).count() <= k) mine.add(v);
+#endif
         }
     } else {
         const int no = open.count();
         for (int i = lane; i < no; i += 32) {  // dp.cpp:51-53: Q(S,w) for every open w
             const int w = nth_member<W>(open, i);
+#if ETWG_K1 == 2
+            rows[w] = c.q(adj, S, w, spill);
+#else
             rows[w] = reach_from<W, false>(adj, S, R, w);
+#endif
         }
         __syncwarp();
         const int ne = eligible.count();

@@ -193,8 +193,17 @@ __device__ __forceinline__ u64 part_of(const Set<W>& key, int lg) {
 }
 
 
+#ifndef ETWG_SCATTER_MINB
+#define ETWG_SCATTER_MINB 0  // >0: ask ptxas for that many resident CTAs per SM (register cap)
+#endif
+#if ETWG_SCATTER_MINB > 0
+#define ETWG_SCATTER_BOUNDS __launch_bounds__(kThreads, ETWG_SCATTER_MINB)
+#else
+#define ETWG_SCATTER_BOUNDS __launch_bounds__(kThreads)
+#endif
+
 template <int W, bool MMW, bool BLOOM>
-__global__ void __launch_bounds__(kThreads) k_exact_scatter(const Params* __restrict__ P, Control* C,
+__global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P, Control* C,
                                                             Bufs B) {
     __shared__ Set<W> adj[64 * W];
     __shared__ unsigned mmw_keep[MMW ? kThreads : 1][2 * W];

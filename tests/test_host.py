@@ -197,3 +197,62 @@ def test_preprocess_errors_do_not_cross_the_abi(E):
     assert lib.etwg_split(200, rows, 2, v, v, v) == -1
     with pytest.raises(ValueError):
         E.max_clique([0] * 200)
+
+
+def _embed(rows, n2, rng, triangle):
+    """G (n <= 64) placed order-preservingly at sorted random positions of an
+    n2-vertex graph; the other vertices are isolated fillers, or (triangle)
+    three of the highest fillers form a triangle."""
+    n = len(rows)
+    pos = sorted(rng.sample(range(n2), n))
+    fill = [p for p in range(n2) if p not in set(pos)]
+    out = [0] * n2
+    for u in range(n):
+        for v in range(n):
+            if rows[u] >> v & 1:
+                out[pos[u]] |= 1 << pos[v]
+    if triangle:
+        a, b, c = fill[-3:]
+        for x, y in ((a, b), (a, c), (b, c)):
+            out[x] |= 1 << y
+            out[y] |= 1 << x
+    return out, pos
+
+
+def _lift(mask, pos):
+    return sum(1 << pos[v] for v in range(len(pos)) if mask >> v & 1)
+
+
+def test_wide_preprocess_matches_reference_after_embedding(E, ref):
+    """f3: the 128-bit host preprocessing keeps the
+    reference's tie-breaking at n > 64. Reference graphs (n <= 64) are
+    embedded order-preservingly into 72..128 vertices (positions spread over
+    both 64-bit words); max_clique (preprocess.cpp:171-184), the
+    vertex-disjoint path counts (:218-243), the improvement edges, the root
+    MMW bound and the split blocks must be the reference's, relabelled."""
+    import random
+    rng = random.Random(11)
+    graphs = [G.random_graph(s * 13 + 5, 20 + s % 45, 0.15 + 0.05 * (s % 5)) for s in range(14)]
+    graphs += [G.queen_graph(6, 6), G.myciel(4), G.grid_graph(7, 9)]
+    for i, rows in enumerate(graphs):
+        n = len(rows)
+        n2 = (72, 96, 128)[i % 3]
+        clique = ref.max_clique(rows)
+        triangle = bin(clique).count("1") >= 4
+        big, pos = _embed(rows, n2, rng, triangle)
+        assert any(p >= 64 for p in pos)
+        assert E.max_clique(big) == _lift(clique, pos), i
+        dp_small, dp_big = ref.disjoint_paths(rows), E.disjoint_paths(big)
+        for u in range(n):
+            for v in range(n):
+                assert dp_big[pos[u] * n2 + pos[v]] == dp_small[u * n + v], (i, u, v)
+        for k in (2, 4, 7):
+            imp_small, imp_big = ref.improve_graph(rows, k), E.improve_graph(big, k)
+            for u in range(n):
+                assert imp_big[pos[u]] == _lift(imp_small[u], pos), (i, k, u)
+        if not triangle:
+            assert E.mmw_lower_bound(big) == ref.mmw_lower_bound(rows)
+        blocks_big = {tuple(v) for v, _ in E.split(big)}
+        for verts, _ in ref.split(rows, 2):
+            if len(verts) > 1:
+                assert tuple(pos[v] for v in verts) in blocks_big, (i, verts)
