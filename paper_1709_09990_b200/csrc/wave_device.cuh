@@ -450,7 +450,8 @@ struct Comps {
     // `targets` outside `reject`)
     __device__ __forceinline__ Set<W> q(const Set<W>* adj, const Set<W>& a, Set<W> q0, int v,
                                         const Spill& spill) const {
-        for_each_any(a & sing, [&](int u) { q0 |= adj[u]; });
+        Set<W> x = a & sing;
+        while (x.any()) q0 |= adj[pop_any(x)];
 #pragma unroll
         for (int j = 0; j < kSlotRegs; ++j)
             if (slot[j].has(v)) q0 |= slot[j];
@@ -473,12 +474,14 @@ __device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, con
     typename Comps<W>::Spill spill;
     c.build(adj, S, eligible, k + 1, spill);  // |Q(S,v)| >= |B_K| - 1 for v in B_K
     Set<W> keep = Set<W>::zero();
-    for_each_any(eligible - c.reject, [&](int v) {
+    // one loop over the candidates (|eligible| is warp-uniform, so no lane
+    // idles), no early exit: the final test implies |N(v) \ S| <= k
+    Set<W> cand = eligible - c.reject;
+    while (cand.any()) {
+        const int v = pop_any(cand);
         const Set<W> a = adj[v];
-        const Set<W> q0 = a - S;
-        if (q0.count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
-        if (c.q(adj, a, q0, v, spill).count() <= k) keep.add(v);
-    });
+        if (c.q(adj, a, a - S, v, spill).count() <= k) keep.add(v);
+    }
     return keep;
 }
 

@@ -40,15 +40,36 @@ def test_myciel4_mmw_acceptance_criterion_4(E, big_goldens, gpu):
     assert ok and w == 10
 
 
-@pytest.mark.slow
 def test_g48_bench_workload_matches_reference(E, gpu):
     """BASELINE cfg 4 (the bench workload): G(48,0.2) seed 1, exact dedup,
-    max_layer_states 2^31 — the reference's full sweep to tw 24."""
+    max_layer_states 2^31 — the full sweep k = 11..24 (2,316,224,115
+    expanded states) against the reference's decide on the same attempts
+    (tests/golden/g48_ref.json, made by tests/golden/make_big_goldens.py on
+    the unmodified reference): block, clique, MMW bound, start k, every
+    attempt's outcome and improvement edges, every round's counters, and the
+    witness of the feasible attempt; treewidth 24."""
     g = g48_golden()
     if g is None:
         pytest.skip("tests/golden/g48_ref.json not generated yet")
-    res = E.solve(E.Graph.from_rows(G.random_graph(1, 48, 0.2)),
-                  E.Options(dedup="exact", max_layer_states=1 << 31,
-                            thread_count=g["options"]["threads"]))
-    assert res.value == g["tw"] == 24
-    assert res.stats_json == g["exact_stats"]
+    rows = G.random_graph(1, 48, 0.2)
+    res = E.solve(E.Graph.from_rows(rows), E.Options(dedup="exact", max_layer_states=1 << 31))
+    assert res.kind == "exact" and res.value == g["tw"] == 24
+    st = json.loads(res.stats_json)
+    comp = max(st["components"], key=lambda c: len(c["vertices"]))
+    assert [v - 1 for v in comp["vertices"]] == g["block"]
+    assert (comp["clique_size"], comp["mmw_bound"], comp["start_k"]) == \
+        (g["clique_size"], g["mmw_bound"], g["start_k"])
+    assert [a["k"] for a in comp["attempts"]] == [a["k"] for a in g["attempts"]]
+    for a, want in zip(comp["attempts"], g["attempts"]):
+        assert (a["outcome"], a["overflowed"], a["added_edges"]) == \
+            (want["outcome"], want["overflowed"], want["added_edges"]), a["k"]
+        got = [[l["round"], l["expanded"], l["emitted"], l["duplicates"], l["mmw_pruned"],
+                l["overflowed"]] for l in a["layers"]]
+        assert got == want["layers"], a["k"]
+    assert st["totals"]["expanded"] == g["expanded"] == 2_316_224_115
+    # the feasible attempt's witness (front() of the last layer, dp.cpp:191-192)
+    sub = [sum(1 << j for j, u in enumerate(g["block"]) if rows[v] >> u & 1) for v in g["block"]]
+    clique = E.max_clique(sub)
+    run = E.decide(E.improve_graph(sub, 24), 24, forbidden=clique, dedup="exact", cap=1 << 31,
+                   keep_layers=False)
+    assert run.outcome == "feasible" and run.witness_set == g["attempts"][-1]["witness"]
