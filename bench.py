@@ -220,6 +220,7 @@ def run_gpu(args):
             "expanded_per_step": total_expanded // max(1, args.steps),
             "treewidth": res.value, "e2e": e2e, "roofline": roof, "gpu_launches": launches,
             "clocks": clk.summary(), "device": info["name"], "shards": shard}
+    line["parity"] = golden_parity(stats)
     if shard["world"] > 1:
         line["exchange_GB_per_step"] = t["exchange_bytes"] / args.steps / 1e9
         line["rerun_rounds"] = int(t["reruns"])
@@ -228,6 +229,27 @@ def run_gpu(args):
         line["cpu_baseline"] = cpu_baseline(rows, stats, budget_s=args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def golden_parity(stats):
+    """The timed solve's stats against the reference's full sweep of the same
+    workload (tests/golden/g48_ref.json, generated from the unmodified
+    reference by tests/golden/make_big_goldens.py): every attempt's outcome,
+    improvement edges and per-round counters, and the treewidth."""
+    import hashlib
+    path = os.path.join(ROOT, "tests", "golden", "g48_ref.json")
+    if not os.path.exists(path):
+        return {"golden": None, "match": None}
+    raw = open(path, "rb").read()
+    g = json.loads(raw)
+    comp = max(stats["components"], key=lambda c: len(c["vertices"]))
+    att = comp["attempts"]
+    match = (stats["result"]["value"] == g["tw"] and len(att) == len(g["attempts"]) and all(
+        (a["k"], a["outcome"], a["added_edges"]) == (w["k"], w["outcome"], w["added_edges"]) and
+        [[l["round"], l["expanded"], l["emitted"], l["duplicates"], l["mmw_pruned"], l["overflowed"]]
+         for l in a["layers"]] == w["layers"] for a, w in zip(att, g["attempts"])))
+    return {"golden": "tests/golden/g48_ref.json", "golden_sha256": hashlib.sha256(raw).hexdigest()[:16],
+            "rounds_compared": sum(len(w["layers"]) for w in g["attempts"]), "match": bool(match)}
 
 
 def roofline(p):

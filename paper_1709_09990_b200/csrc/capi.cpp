@@ -428,7 +428,9 @@ int etwg_times(double* out, int len) {
                         t.insert_bytes,
                         t.append_bytes,
                         static_cast<double>(t.offered),
-                        static_cast<double>(t.unique)};
+                        static_cast<double>(t.unique),
+                        static_cast<double>(t.bloom_probed),
+                        static_cast<double>(t.bloom_fp)};
     int n = static_cast<int>(sizeof v / sizeof v[0]);
     if (len < n) n = len;
     for (int i = 0; i < n; ++i) out[i] = v[i];

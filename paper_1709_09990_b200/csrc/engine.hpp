@@ -129,6 +129,8 @@ struct KernelTimes {
     // insert / partition dedup, append
     double expand_bytes = 0, insert_bytes = 0, append_bytes = 0;
     uint64_t offered = 0, unique = 0;  // children offered to dedup / distinct children
+    // partitioned Bloom rounds: distinct keys probed / rejected by the filter
+    uint64_t bloom_probed = 0, bloom_fp = 0;
 };
 // Brackets a region on the engine's stream with CUDA events; end returns the
 // device milliseconds between the two events (synchronizing).

@@ -59,6 +59,8 @@ struct RoundStats {
     u64 winners;  // exact mode: children left after the tile pre-dedup
     u64 np;       // exact mode: partitions of the round (power of two)
     u64 pcap;     // exact mode: record capacity per partition
+    u64 probed;   // partitioned Bloom: distinct keys sent through the filter
+    u64 fp;       // partitioned Bloom: of those, rejected by the filter (false positives)
     unsigned overflowed, valid;
 };
 
@@ -85,6 +87,9 @@ struct Control {
     unsigned handed, pad2;
     u64 part_floor;     // exact mode: minimum partitions after a grow (per decide)
     u64 rec_floor;      // exact mode: minimum records per partition after a grow
+    unsigned fp_log_n;  // ETWG_DEBUG 2048: first false positives logged (key, h1, h2, m)
+    unsigned pad3;
+    u64 fp_log[16][4];
     RoundStats rs[kMaxRounds];
 };
 
@@ -450,7 +455,22 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
                 const unsigned h2 = murmur_key<W>(key, kSeed2);
                 u64 pos, step;
                 probe_start(h1, h2, m, pos, step);
-                if (!bloom_or_probes(bits, m, pos, step, P->hashes)) continue;
+                atomicAdd(&C->rs[r].probed, 1ull);
+                if (!bloom_or_probes(bits, m, pos, step, P->hashes)) {
+                    // a distinct key of the round whose probe bits were all set
+                    // by other keys: a false positive (the reference drops it too)
+                    atomicAdd(&C->rs[r].fp, 1ull);
+                    if (P->flags & 2048) {
+                        const unsigned at = atomicAdd(&C->fp_log_n, 1u);
+                        if (at < 16) {
+                            C->fp_log[at][0] = key.w[0];
+                            C->fp_log[at][1] = W == 2 ? key.w[W - 1] : 0;
+                            C->fp_log[at][2] = (static_cast<u64>(h1) << 32) | h2;
+                            C->fp_log[at][3] = m;
+                        }
+                    }
+                    continue;
+                }
             }
             const u64 parent = rank / (64 * W);
             const int v = static_cast<int>(rank % (64 * W));
@@ -811,7 +831,19 @@ public:
             ls.overflowed = s.overflowed != 0;
             any_ovf = any_ovf || ls.overflowed;
             res.rounds.push_back(ls);
+            prof.t.bloom_probed += s.probed;
+            prof.t.bloom_fp += s.fp;
+            if (s.fp && std::getenv("ETWG_TRACE"))
+                std::fprintf(stderr, "[engine] k=%d round %d: %llu of %llu distinct keys rejected by the filter\n", k, r,
+                             static_cast<unsigned long long>(s.fp), static_cast<unsigned long long>(s.probed));
             if (s.emitted == 0) break;
+        }
+        if ((h_params_->flags & 2048) && c.fp_log_n) {
+            for (unsigned i = 0; i < std::min(c.fp_log_n, 16u); ++i)
+                std::fprintf(stderr, "[fp] k=%d key=%016llx:%016llx h1=%08x h2=%08x m=%llu\n", k,
+                             static_cast<unsigned long long>(c.fp_log[i][1]), static_cast<unsigned long long>(c.fp_log[i][0]),
+                             static_cast<unsigned>(c.fp_log[i][2] >> 32), static_cast<unsigned>(c.fp_log[i][2]),
+                             static_cast<unsigned long long>(c.fp_log[i][3]));
         }
         res.overflowed = any_ovf;
         account(res.rounds, W, cfg);

@@ -23,6 +23,9 @@ built from /root/reference/proj/src by `make -C oracle ref`) through its own
         fit a call; the prebuilt .so travels, the reference tree is not read
         there.
 
+    python tests/golden/make_big_goldens.py queen88
+        queen8_8 (n = 64, tw 45) exact with the order, ~6 min on 8 cores.
+
     python tests/golden/make_big_goldens.py g48-merge
         Merges the pieces and the cheap solve() prelude computed here (block,
         clique, MMW bound, start k, improvement edges per k) into
@@ -82,6 +85,25 @@ def small() -> None:
     with open(path, "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
     print("wrote", path)
+
+
+def queen88() -> None:
+    """queen8_8 (n = 64: the full 64-bit word; tw 45), exact
+    dedup with max_layer_states 2^31 (the default 10M would overflow), with
+    the elimination order: merged into big_goldens.json."""
+    ref = RefLib()
+    rows = G.queen_graph(8, 8)
+    t = time.time()
+    ex = ref.solve(rows, dedup="exact", threads=os.cpu_count(), cap=BIG_CAP, emit_order=True,
+                   json_len=1 << 26)
+    path = os.path.join(HERE, "big_goldens.json")
+    out = json.load(open(path))
+    out["queen8_8"] = {"tw": ex["value"], "kind": ex["kind"], "threads": os.cpu_count(),
+                       "max_layer_states": BIG_CAP, "order": ex["order"], "exact_stats": ex["stats"],
+                       "ref_s": round(time.time() - t, 1)}
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print("queen8_8 tw", ex["value"], "in", round(time.time() - t, 1), "s")
 
 
 def _g48_block(ref):
@@ -161,5 +183,7 @@ if __name__ == "__main__":
         g48(int(sys.argv[2]), [int(x) for x in sys.argv[3:]])
     elif what == "g48-merge":
         g48_merge()
+    elif what == "queen88":
+        queen88()
     else:
         raise SystemExit(f"unknown target {what}")

@@ -154,10 +154,10 @@ def test_sharded_128bit_large_shard_layers(E, shards):
     tile-status array covers 4096 tiles of 1024 parents at W = 2): counters
     equal the single-device engine's."""
     rows = G.random_graph(3, 70, 0.5)
-    want = E.decide(rows, 60, dedup="exact", rounds=4, cap=1 << 31, keep_layers=False)
+    want = E.decide(rows, 60, dedup="exact", rounds=6, cap=1 << 31, keep_layers=False)
     assert want.rounds[-1].emitted > 2 * 4096 * 1024
     shards(2)
-    got = E.decide(rows, 60, dedup="exact", rounds=4, cap=1 << 31, keep_layers=False)
+    got = E.decide(rows, 60, dedup="exact", rounds=6, cap=1 << 31, keep_layers=False)
     assert _counters(got) == _counters(want)
     assert got.outcome == want.outcome
 
