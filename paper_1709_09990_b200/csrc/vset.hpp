@@ -46,9 +46,15 @@ struct Set {
         for (int i = 0; i < W; ++i) s.w[i] = 0;
         return s;
     }
+    // Single-bit access selects the word with constant indices (an unrolled
+    // compare per word) instead of w[v >> 6]: a runtime index into w[] makes
+    // nvcc keep the whole set, and every set stored next to it, in local
+    // memory.
     ETW_HD static Set bit(int v) {
-        Set s = zero();
-        s.w[v >> 6] = uint64_t{1} << (v & 63);
+        Set s;
+        const uint64_t b = uint64_t{1} << (v & 63);
+#pragma unroll
+        for (int i = 0; i < W; ++i) s.w[i] = (W == 1 || (v >> 6) == i) ? b : 0;
         return s;
     }
     // {0..n-1}
@@ -61,9 +67,26 @@ struct Set {
         }
         return s;
     }
-    ETW_HD bool has(int v) const { return (w[v >> 6] >> (v & 63)) & 1u; }
-    ETW_HD void add(int v) { w[v >> 6] |= uint64_t{1} << (v & 63); }
-    ETW_HD void del(int v) { w[v >> 6] &= ~(uint64_t{1} << (v & 63)); }
+    ETW_HD uint64_t word_of(int v) const {
+        uint64_t x = w[0];
+#pragma unroll
+        for (int i = 1; i < W; ++i)
+            if ((v >> 6) == i) x = w[i];
+        return x;
+    }
+    ETW_HD bool has(int v) const { return (word_of(v) >> (v & 63)) & 1u; }
+    ETW_HD void add(int v) {
+        const uint64_t b = uint64_t{1} << (v & 63);
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (W == 1 || (v >> 6) == i) w[i] |= b;
+    }
+    ETW_HD void del(int v) {
+        const uint64_t b = uint64_t{1} << (v & 63);
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (W == 1 || (v >> 6) == i) w[i] &= ~b;
+    }
     ETW_HD int count() const {
         int c = 0;
 #pragma unroll

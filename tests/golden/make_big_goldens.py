@@ -26,6 +26,10 @@ built from /root/reference/proj/src by `make -C oracle ref`) through its own
     python tests/golden/make_big_goldens.py queen88
         queen8_8 (n = 64, tw 45) exact with the order, ~6 min on 8 cores.
 
+    python tests/golden/make_big_goldens.py grid88
+        8x8 grid + 6 chords (n = 64, default cap: overflow -> lower bound),
+        ~20 min on 8 cores.
+
     python tests/golden/make_big_goldens.py g48-merge
         Merges the pieces and the cheap solve() prelude computed here (block,
         clique, MMW bound, start k, improvement edges per k) into
@@ -104,6 +108,24 @@ def queen88() -> None:
     with open(path, "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
     print("queen8_8 tw", ex["value"], "in", round(time.time() - t, 1), "s")
+
+
+def grid88() -> None:
+    """BASELINE cfg 5a: 8x8 grid + 6 chords (seed 7), n = 64 on the one-word
+    path, exact dedup with the reference's default 10M layer cap: the layers
+    overflow (truncation to the lowest emission ranks, dp.cpp:152-155) and the
+    solve returns the lower bound. Merged into big_goldens.json."""
+    ref = RefLib()
+    rows = G.grid_with_chords(8, 8, 6, 7)
+    t = time.time()
+    ex = ref.solve(rows, dedup="exact", threads=os.cpu_count(), json_len=1 << 26)
+    path = os.path.join(HERE, "big_goldens.json")
+    out = json.load(open(path))
+    out["grid8x8_chords6_seed7"] = {"tw": ex["value"], "kind": ex["kind"], "threads": os.cpu_count(),
+                                    "exact_stats": ex["stats"], "ref_s": round(time.time() - t, 1)}
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print("grid 8x8+6", ex["kind"], ex["value"], "in", round(time.time() - t, 1), "s")
 
 
 def _g48_block(ref):
@@ -185,5 +207,7 @@ if __name__ == "__main__":
         g48_merge()
     elif what == "queen88":
         queen88()
+    elif what == "grid88":
+        grid88()
     else:
         raise SystemExit(f"unknown target {what}")

@@ -73,3 +73,32 @@ def test_g48_bench_workload_matches_reference(E, gpu):
     run = E.decide(E.improve_graph(sub, 24), 24, forbidden=clique, dedup="exact", cap=1 << 31,
                    keep_layers=False)
     assert run.outcome == "feasible" and run.witness_set == g["attempts"][-1]["witness"]
+
+
+def test_queen8_8_full_word(E, big_goldens, gpu):
+    """n = 64 (every bit of the one-word key in use): queen8_8, tw 45
+    (PAPER.md:165), exact with max_layer_states 2^31; stats JSON and the
+    reconstructed order byte-identical to the reference's."""
+    g = big_goldens["queen8_8"]
+    graph = E.Graph.from_rows(G.queen_graph(8, 8))
+    res = E.solve(graph, E.Options(dedup="exact", max_layer_states=1 << 31, emit_order=True,
+                                   thread_count=g["threads"]))
+    assert res.kind == "exact" and res.value == g["tw"] == 45
+    assert res.stats_json == g["exact_stats"]
+    assert res.order == g["order"]
+    w, ok = graph.check_order(res.order)
+    assert ok and w == 45
+
+
+def test_grid8x8_chords_lower_bound(E, big_goldens, gpu):
+    """BASELINE cfg 5a: 8x8 grid + 6 chords (n = 64) with the default 10M
+    layer cap. Layers overflow, truncation keeps the lowest emission ranks
+    (dp.cpp:152-155) and the solve returns the reference's lower bound; the
+    whole stats JSON (every truncated round) is byte-identical."""
+    g = big_goldens.get("grid8x8_chords6_seed7")
+    if g is None:
+        pytest.skip("grid88 golden not generated")
+    res = E.solve(E.Graph.from_rows(G.grid_with_chords(8, 8, 6, 7)),
+                  E.Options(dedup="exact", thread_count=g["threads"]))
+    assert (res.kind, res.value) == (g["kind"], g["tw"])
+    assert res.stats_json == g["exact_stats"]
