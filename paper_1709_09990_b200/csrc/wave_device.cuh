@@ -384,6 +384,9 @@ __device__ __forceinline__ Set<W> candidates_shared(const Set<W>* adj, int k, co
 #ifndef ETWG_K1
 #define ETWG_K1 2  // 2: register boundary slots; 1: per-vertex table (component_reach)
 #endif
+#ifndef ETWG_K1_LOOP
+#define ETWG_K1_LOOP 2  // 1: two 32-bit half loops with an early |N(v) \ S| > k exit
+#endif
 #ifndef ETWG_SLOT_REGS
 #define ETWG_SLOT_REGS 4
 #endif
@@ -474,6 +477,14 @@ __device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, con
     typename Comps<W>::Spill spill;
     c.build(adj, S, eligible, k + 1, spill);  // |Q(S,v)| >= |B_K| - 1 for v in B_K
     Set<W> keep = Set<W>::zero();
+#if ETWG_K1_LOOP == 1
+    for_each_any(eligible - c.reject, [&](int v) {
+        const Set<W> a = adj[v];
+        const Set<W> q0 = a - S;
+        if (q0.count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
+        if (c.q(adj, a, q0, v, spill).count() <= k) keep.add(v);
+    });
+#else
     // one loop over the candidates (|eligible| is warp-uniform, so no lane
     // idles), no early exit: the final test implies |N(v) \ S| <= k
     Set<W> cand = eligible - c.reject;
@@ -482,6 +493,7 @@ __device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, con
         const Set<W> a = adj[v];
         if (c.q(adj, a, a - S, v, spill).count() <= k) keep.add(v);
     }
+#endif
     return keep;
 }
 
