@@ -138,6 +138,9 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_APPEND_MINB
 #define ETWG_APPEND_MINB 4  // k_append: >= 4 resident CTAs per SM (registers <= 64)
 #endif
+#ifndef ETWG_EMIT_FLAT
+#define ETWG_EMIT_FLAT 1  // 1: children flattened over the warp's lanes; 0: each lane emits its own
+#endif
 #ifndef ETWG_EMIT_UNROLL
 #define ETWG_EMIT_UNROLL 2  // children emitted per lane per step in k_exact_scatter
 #endif
@@ -310,9 +313,46 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         offered += M.count();
         winners += M.count();
         if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
+        bool full = false;
+#if ETWG_EMIT_FLAT == 0
+        // each lane emits its own parent's children, two per step so both
+        // bucket-cursor atomics are in flight together; no flattening
+        // shuffles (the trip count is the warp's largest child count)
+        {
+            Set<W> rest = M;
+            while (rest.any()) {
+                Set<W> key[2];
+                u64 part[2], rank[2];
+                unsigned slot[2] = {~0u, ~0u};
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (!rest.any()) break;
+                    const int v = pop_any(rest);
+                    key[u] = S;
+                    key[u].add(v);
+                    part[u] = part_of<W>(key[u], pl.lg);
+                    rank[u] = child_rank<W>(idx, v);
+                    slot[u] = atomicAdd(B.cursors + part[u], 1u);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (slot[u] == ~0u) continue;
+                    if (slot[u] < pl.cap) {
+                        u64* rec = B.recs + (part[u] * pl.cap + slot[u]) * rec_words<W>();
+                        if constexpr (W == 1) {
+                            *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key[u].w[0], rank[u]);
+                        } else {
+                            *reinterpret_cast<ulonglong4*>(rec) = make_ulonglong4(key[u].w[0], key[u].w[1], rank[u], 0);
+                        }
+                    } else {
+                        full = true;
+                    }
+                }
+            }
+        }
+#else
         WarpFlat f;
         f.scan(M.count());
-        bool full = false;
         // ETWG_EMIT_UNROLL children per lane per step: their bucket-cursor
         // atomics are in flight together instead of one round trip each
         constexpr int U = ETWG_EMIT_UNROLL;
@@ -351,6 +391,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 }
             }
         }
+#endif
         if (__any_sync(kFull, full) && lane == 0) {
             C->need = 2 * pl.cap;
             C->abort = kGrowRecs;
@@ -1430,10 +1471,18 @@ private:
             case kGrowLayer:
                 ensure_layers(c.need + c.need / 2, static_cast<int>(r & 1), c.count[r & 1]);
                 break;
-            case kGrowParts:
-                c.part_floor = std::max<u64>(c.part_floor, c.need);
+            case kGrowParts: {
+                // more partitions: each gets proportionally fewer records, so a
+                // record floor raised at the old partition count shrinks with it
+                // (a fixed floor times a doubling partition count grew the record
+                // buffer without bound under repeated table overflows)
+                const u64 np_old = std::max<u64>(c.rs[r].np, 1);
+                const u64 np_new = std::max<u64>(c.part_floor, c.need);
+                if (np_new > np_old) c.rec_floor = c.rec_floor * np_old / np_new;
+                c.part_floor = np_new;
                 clean_cursors();
                 break;
+            }
             case kGrowRecs:
                 c.rec_floor = std::max<u64>(c.rec_floor, c.need);
                 clean_cursors();

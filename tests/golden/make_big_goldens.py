@@ -30,6 +30,10 @@ built from /root/reference/proj/src by `make -C oracle ref`) through its own
         8x8 grid + 6 chords (n = 64, default cap: overflow -> lower bound),
         ~20 min on 8 cores.
 
+    python tests/golden/make_big_goldens.py wide72
+        G(72,0.5) seed 1 on the 128-bit path (oracle checker; no reference
+        above 64 vertices).
+
     python tests/golden/make_big_goldens.py g48-merge
         Merges the pieces and the cheap solve() prelude computed here (block,
         clique, MMW bound, start k, improvement edges per k) into
@@ -128,6 +132,46 @@ def grid88() -> None:
     print("grid 8x8+6", ex["kind"], ex["value"], "in", round(time.time() - t, 1), "s")
 
 
+def wide72() -> None:
+    """BASELINE cfg 5b, the 128-bit path to an exact treewidth: G(72,0.5)
+    seed 1 (tw 57, ~7.4M expanded states). No reference exists above 64
+    vertices (graph.cpp:111-113), so the checker is the oracle's decide
+    (oracle/etw_oracle.c, 128-bit sets) on every attempt solve() makes:
+    the block, the forbidden max clique and the improved graph per k come
+    from the host preprocessing (tested against the reference by embedding,
+    tests/test_host.py). Merged into big_goldens.json."""
+    from checkers import Oracle
+    from paper_1709_09990_b200 import elimtw as E
+    oracle = Oracle()
+    rows = G.random_graph(1, 72, 0.5)
+    blocks = E.split(rows)
+    verts = max(blocks, key=lambda b: len(b[0]))[0]
+    sub = [sum(1 << j for j, u in enumerate(verts) if rows[v] >> u & 1) for v in verts]
+    clique = E.max_clique(sub)
+    k = max(bin(clique).count("1") - 1, E.mmw_lower_bound(sub))
+    attempts = []
+    t = time.time()
+    while True:
+        gk = E.improve_graph(sub, k)
+        run = oracle.decide(gk, k, forbidden=clique, dedup="exact", cap=BIG_CAP, keep_layers=False)
+        attempts.append({"k": k, "outcome": run.outcome, "witness": [run.witness_set & (2**64 - 1),
+                                                                     run.witness_set >> 64],
+                         "layers": [[x.round, x.expanded, x.emitted, x.duplicates, x.mmw_pruned,
+                                     bool(x.overflowed)] for x in run.rounds]})
+        print("k", k, run.outcome, sum(x.expanded for x in run.rounds), flush=True)
+        if run.outcome == "feasible":
+            break
+        k += 1
+    path = os.path.join(HERE, "big_goldens.json")
+    out = json.load(open(path))
+    out["g72_05_seed1"] = {"checker": "oracle decide per attempt (128-bit)", "block": verts,
+                           "clique": [clique & (2**64 - 1), clique >> 64], "tw": k,
+                           "attempts": attempts, "oracle_s": round(time.time() - t, 1)}
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print("G(72,0.5) tw", k, "in", round(time.time() - t, 1), "s")
+
+
 def _g48_block(ref):
     rows = G.random_graph(1, 48, 0.2)
     blocks = ref.split(rows, 2)
@@ -209,5 +253,7 @@ if __name__ == "__main__":
         queen88()
     elif what == "grid88":
         grid88()
+    elif what == "wide72":
+        wide72()
     else:
         raise SystemExit(f"unknown target {what}")

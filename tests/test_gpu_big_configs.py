@@ -103,3 +103,27 @@ def test_grid8x8_chords_lower_bound(E, big_goldens, gpu):
     assert g["kind"] == "lower_bound_only" and res.kind == "lower_bound"  # ETW_RESULT_LOWER_BOUND_ONLY
     assert res.value == g["tw"]
     assert res.stats_json == g["exact_stats"]
+
+
+def test_g72_128bit_path_exact(E, big_goldens, gpu):
+    """BASELINE cfg 5b: a 72-vertex instance solved to its exact treewidth on
+    the 128-bit path, G(72,0.5) seed 1 (tw 57). Every attempt's outcome and
+    per-round counters equal the oracle's decide (no reference above 64
+    vertices); the reconstructed order validates to width 57."""
+    g = big_goldens.get("g72_05_seed1")
+    if g is None:
+        pytest.skip("wide72 golden not generated")
+    graph = E.Graph.from_rows(G.random_graph(1, 72, 0.5))
+    res = E.solve(graph, E.Options(dedup="exact", max_layer_states=1 << 31, emit_order=True))
+    assert res.kind == "exact" and res.value == g["tw"] == 57
+    st = json.loads(res.stats_json)
+    comp = max(st["components"], key=lambda c: len(c["vertices"]))
+    assert [v - 1 for v in comp["vertices"]] == g["block"]
+    assert [(a["k"], a["outcome"]) for a in comp["attempts"]] == \
+        [(a["k"], a["outcome"]) for a in g["attempts"]]
+    for a, want in zip(comp["attempts"], g["attempts"]):
+        got = [[l["round"], l["expanded"], l["emitted"], l["duplicates"], l["mmw_pruned"],
+                l["overflowed"]] for l in a["layers"]]
+        assert got == want["layers"], a["k"]
+    w, ok = graph.check_order(res.order)
+    assert ok and w == 57
