@@ -62,6 +62,7 @@ struct RoundStats {
     u64 probed;   // partitioned Bloom: distinct keys sent through the filter
     u64 fp;       // partitioned Bloom: of those, rejected by the filter (false positives)
     unsigned overflowed, valid;
+    unsigned compact, nb;  // exact mode: 8-byte records this round (PartPlan)
 };
 
 enum AbortCode : unsigned {
@@ -166,9 +167,59 @@ __device__ __forceinline__ u64 ceil_pow2(u64 x) {
     return s;
 }
 
+// Compact 8-byte records (n <= 64, one-word keys). The key is replaced by an
+// n-bit bijective mix m = mixn(key); the bucket is the top lg bits of m, so a
+// record only carries the low nb = n - lg bits of m plus the 32-bit parent
+// index: {low << 32 | parent}. Among emissions of one key the minimum
+// emission rank idx*64+v (dp.cpp:66) is the minimum parent index (one key
+// comes at most once from each parent), so the parent index is the rank; v
+// is recovered as the one bit of key \ S[parent] when the winner is marked.
+// Needs nb <= 31 (the 32-bit table key 0xFFFFFFFF means empty) and layers
+// below 2^32 states; other rounds keep the 16-byte {key, rank} records.
+constexpr u64 kMixC1 = 0xff51afd7ed558ccdULL;
+constexpr u64 kMixC2 = 0xc4ceb9fe1a85ec53ULL;
+__host__ __device__ constexpr u64 inv_odd(u64 c) {
+    u64 x = c;  // Newton: x <- x (2 - c x) doubles the correct low bits
+    for (int i = 0; i < 6; ++i) x *= 2 - c * x;
+    return x;
+}
+constexpr u64 kMixC1inv = inv_odd(kMixC1);
+constexpr u64 kMixC2inv = inv_odd(kMixC2);
+static_assert(kMixC1 * kMixC1inv == 1 && kMixC2 * kMixC2inv == 1, "modular inverses");
+
+__device__ __forceinline__ u64 nmask(int n) { return n >= 64 ? ~u64{0} : (u64{1} << n) - 1; }
+
+// x ^= x >> s with 2s >= n is an involution on n-bit values
+__device__ __forceinline__ u64 mixn(u64 x, int n) {
+    const int s = (n + 1) >> 1;
+    const u64 m = nmask(n);
+    x ^= x >> s;
+    x = (x * kMixC1) & m;
+    x ^= x >> s;
+    x = (x * kMixC2) & m;
+    x ^= x >> s;
+    return x;
+}
+
+__device__ __forceinline__ u64 unmixn(u64 x, int n) {
+    const int s = (n + 1) >> 1;
+    const u64 m = nmask(n);
+    x ^= x >> s;
+    x = (x * kMixC2inv) & m;
+    x ^= x >> s;
+    x = (x * kMixC1inv) & m;
+    x ^= x >> s;
+    return x;
+}
+
+constexpr int kCompactSlots = 4096;  // 32-bit key + 32-bit parent per slot: 32 KB
+constexpr int compact_smem_bytes() { return kCompactSlots * 8; }
+
 struct PartPlan {
     u64 np, cap;
     int lg;
+    int compact;  // 8-byte records this round
+    int nb;       // bits of the mixed key a compact record carries (n - lg)
 };
 
 template <int W>
@@ -189,6 +240,18 @@ __device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C,
     if (pl.np < C->part_floor) pl.np = C->part_floor;
     pl.lg = 0;
     while ((u64{1} << pl.lg) < pl.np) ++pl.lg;
+    pl.compact = 0;
+    pl.nb = 0;
+    if (W == 1 && !(P->flags & 4096) && E <= 0xFFFFFFFFull) {  // ETWG_DEBUG 4096: 16-byte records only
+        // up to 4x the planned buckets to bring the record's key bits to 31
+        const int need = P->n - 31 > pl.lg ? P->n - 31 : pl.lg;
+        if (need - pl.lg <= 2) {
+            pl.np <<= need - pl.lg;
+            pl.lg = need;
+            pl.compact = 1;
+            pl.nb = P->n - pl.lg;
+        }
+    }
     const u64 per = (winners + pl.np - 1) / pl.np;
     pl.cap = tight ? per / 4 + 1 : per + per / 4 + 64;
     if (pl.cap < C->rec_floor) pl.cap = C->rec_floor;
@@ -198,6 +261,33 @@ __device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C,
 template <int W>
 __device__ __forceinline__ u64 part_of(const Set<W>& key, int lg) {
     return lg ? slot_hash<W>(key) >> (64 - lg) : 0;
+}
+
+// Bucket of a child, and (compact rounds) the record's mixed-key low bits.
+template <int W>
+__device__ __forceinline__ u64 record_part(const Set<W>& key, const PartPlan& pl, int n, u64& low) {
+    if (W == 1 && pl.compact) {
+        const u64 m = mixn(key.w[0], n);
+        low = m & nmask(pl.nb);
+        return pl.nb >= 64 ? 0 : m >> pl.nb;
+    }
+    low = 0;
+    return part_of<W>(key, pl.lg);
+}
+
+template <int W>
+__device__ __forceinline__ void record_store(const Bufs& B, const PartPlan& pl, u64 part, unsigned slot,
+                                             const Set<W>& key, u64 low, u64 parent, int v) {
+    if (W == 1 && pl.compact) {
+        B.recs[part * pl.cap + slot] = (low << 32) | parent;
+        return;
+    }
+    u64* rec = B.recs + (part * pl.cap + slot) * rec_words<W>();
+    if constexpr (W == 1) {
+        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(parent, v));
+    } else {
+        *reinterpret_cast<ulonglong4*>(rec) = make_ulonglong4(key.w[0], key.w[1], child_rank<W>(parent, v), 0);
+    }
 }
 
 
@@ -215,6 +305,11 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                                                             Bufs B) {
     __shared__ Set<W> adj[64 * W];
     __shared__ unsigned mmw_keep[MMW ? kThreads : 1][2 * W];
+    // ETWG_K1 3: per-thread component boundaries and vertex signatures
+    // (candidates_sig), dynamic shared memory, zeroed once per launch
+    extern __shared__ __align__(16) unsigned char scatter_dyn[];
+    u64* sig_bs = reinterpret_cast<u64*>(scatter_dyn);
+    unsigned short* sig_tab = reinterpret_cast<unsigned short*>(sig_bs + kSigComps * kThreads);
     __shared__ Set<W> warp_tables[kThreads / 32][MMW ? 2 : 1][64 * W];  // small-layer mode
     if (halted(C)) return;
     const unsigned r = C->round;
@@ -252,11 +347,16 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         C->rs[r].np = pl.np;
         C->rs[r].pcap = pl.cap;
+        C->rs[r].compact = pl.compact;
+        C->rs[r].nb = pl.nb;
     }
+    const int n = P->n;
     const int lane = threadIdx.x & 31;
     const Set<W> forbidden = param_set<W>(P->forbidden);
     const u64* in = B.keys[r & 1];
     load_adjacency<W>(P, adj);
+    if constexpr (W == 1 && !MMW && ETWG_K1 == 3)
+        for (int i = threadIdx.x; i < 64 * kThreads; i += blockDim.x) sig_tab[i] = 0;
     __syncthreads();
     // warp-granular: no block barrier inside the loop, so a warp whose
     // parents are cheap never waits for the CTA's slowest warp
@@ -283,19 +383,13 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 const int v = nth_member<W>(M, i);
                 Set<W> key = S;
                 key.add(v);
-                const u64 part = part_of<W>(key, pl.lg);
+                u64 low;
+                const u64 part = record_part<W>(key, pl, n, low);
                 const unsigned slot = atomicAdd(B.cursors + part, 1u);
-                if (slot < pl.cap) {
-                    u64* rec = B.recs + (part * pl.cap + slot) * rec_words<W>();
-                    if constexpr (W == 1) {
-                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(p, v));
-                    } else {
-                        *reinterpret_cast<ulonglong4*>(rec) =
-                            make_ulonglong4(key.w[0], key.w[1], child_rank<W>(p, v), 0);
-                    }
-                } else {
+                if (slot < pl.cap)
+                    record_store<W>(B, pl, part, slot, key, low, p, v);
+                else
                     full = true;
-                }
             }
         }
         if (__any_sync(kFull, full) && lane == 0) {
@@ -309,7 +403,16 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         const u64 idx = base + lane;
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        const Set<W> M = warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
+        Set<W> M;
+        if constexpr (W == 1 && !MMW && ETWG_K1 == 3) {
+            M = Set<W>::zero();
+            if (valid) {
+                const Set<1> open = Set<1>::prefix(P->n) - S;
+                M = candidates_sig(adj, P->k, S, open - forbidden, sig_bs, sig_tab);
+            }
+        } else {
+            M = warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
+        }
         offered += M.count();
         winners += M.count();
         if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
@@ -322,31 +425,25 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
             Set<W> rest = M;
             while (rest.any()) {
                 Set<W> key[2];
-                u64 part[2], rank[2];
+                u64 part[2], low[2];
+                int vv[2];
                 unsigned slot[2] = {~0u, ~0u};
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                     if (!rest.any()) break;
-                    const int v = pop_any(rest);
+                    vv[u] = pop_any(rest);
                     key[u] = S;
-                    key[u].add(v);
-                    part[u] = part_of<W>(key[u], pl.lg);
-                    rank[u] = child_rank<W>(idx, v);
+                    key[u].add(vv[u]);
+                    part[u] = record_part<W>(key[u], pl, n, low[u]);
                     slot[u] = atomicAdd(B.cursors + part[u], 1u);
                 }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                     if (slot[u] == ~0u) continue;
-                    if (slot[u] < pl.cap) {
-                        u64* rec = B.recs + (part[u] * pl.cap + slot[u]) * rec_words<W>();
-                        if constexpr (W == 1) {
-                            *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key[u].w[0], rank[u]);
-                        } else {
-                            *reinterpret_cast<ulonglong4*>(rec) = make_ulonglong4(key[u].w[0], key[u].w[1], rank[u], 0);
-                        }
-                    } else {
+                    if (slot[u] < pl.cap)
+                        record_store<W>(B, pl, part[u], slot[u], key[u], low[u], idx, vv[u]);
+                    else
                         full = true;
-                    }
                 }
             }
         }
@@ -358,7 +455,8 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         constexpr int U = ETWG_EMIT_UNROLL;
         for (int t = 0; t < f.total; t += 32 * U) {
             Set<W> key[U];
-            u64 part[U], rank[U];
+            u64 part[U], low[U];
+            int vv[U], srcs[U];
             unsigned slot[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -368,27 +466,21 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 const Set<W> Ms = shfl_set<W>(M, src);
                 key[u] = shfl_set<W>(S, src);
                 slot[u] = ~0u;
+                srcs[u] = src;
                 if (j < f.total) {
-                    const int v = nth_member<W>(Ms, j - excl);
-                    key[u].add(v);
-                    part[u] = part_of<W>(key[u], pl.lg);
-                    rank[u] = child_rank<W>(base + src, v);
+                    vv[u] = nth_member<W>(Ms, j - excl);
+                    key[u].add(vv[u]);
+                    part[u] = record_part<W>(key[u], pl, n, low[u]);
                     slot[u] = atomicAdd(B.cursors + part[u], 1u);
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (slot[u] == ~0u) continue;
-                if (slot[u] < pl.cap) {
-                    u64* rec = B.recs + (part[u] * pl.cap + slot[u]) * rec_words<W>();
-                    if constexpr (W == 1) {
-                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key[u].w[0], rank[u]);
-                    } else {
-                        *reinterpret_cast<ulonglong4*>(rec) = make_ulonglong4(key[u].w[0], key[u].w[1], rank[u], 0);
-                    }
-                } else {
+                if (slot[u] < pl.cap)
+                    record_store<W>(B, pl, part[u], slot[u], key[u], low[u], base + srcs[u], vv[u]);
+                else
                     full = true;
-                }
             }
         }
 #endif
@@ -412,6 +504,10 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
 
 constexpr int kPartThreads = 512;
 
+// dynamic shared memory of k_exact_scatter<W, false, *> (candidates_sig tables)
+template <int W>
+constexpr int scatter_smem() { return W == 1 && ETWG_K1 == 3 ? sig_smem_bytes(kThreads) : 0; }
+
 // BLOOM: the round's distinct keys then meet the reference's Bloom filter
 // (bit positions (h1 + i*h2) mod m, bloom.cpp:86-97), each exactly once, so
 // "any probed bit was clear" is the novelty test; keys the filter calls
@@ -425,6 +521,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
     __shared__ unsigned s_full;
     if (halted(C)) return;
     const unsigned r = C->round;
+    if (W == 1 && C->rs[r].compact) return;  // k_exact_part_compact's round
     const u64 np = C->rs[r].np;
     const u64 cap = C->rs[r].pcap;
     for (u64 part = blockIdx.x; part < np; part += gridDim.x) {
@@ -516,6 +613,111 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
             const u64 parent = rank / (64 * W);
             const int v = static_cast<int>(rank % (64 * W));
             atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + parent * W + (v >> 6), u64{1} << (v & 63));
+        }
+        if (threadIdx.x == 0) B.cursors[part] = 0;  // clean for the next round
+        __syncthreads();
+    }
+}
+
+// Compact rounds (8-byte records {low << 32 | parent}, see PartPlan): the
+// same per-bucket min-rank dedup as k_exact_part with a 32-bit key (the
+// mixed key's low bits; the bucket fixes the rest) and the parent index as
+// the rank, in a 32 KB table. The winner's vertex is the one bit of
+// key \ S[parent]: one read of the parent's set per distinct key.
+template <bool BLOOM>
+__global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Params* __restrict__ P, Control* C,
+                                                                     Bufs B) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int SLOTS = kCompactSlots;
+    unsigned* keys = reinterpret_cast<unsigned*>(smem_raw);
+    unsigned* ranks = keys + SLOTS;
+    __shared__ unsigned s_full;
+    if (halted(C)) return;
+    const unsigned r = C->round;
+    if (!C->rs[r].compact) return;
+    const u64 np = C->rs[r].np;
+    const u64 cap = C->rs[r].pcap;
+    const int nb = static_cast<int>(C->rs[r].nb);
+    const int n = P->n;
+    const u64* layer = B.keys[r & 1];
+    for (u64 part = blockIdx.x; part < np; part += gridDim.x) {
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+            keys[i] = ~0u;
+            ranks[i] = ~0u;
+        }
+        if (threadIdx.x == 0) s_full = 0;
+        __syncthreads();
+        const unsigned cnt = B.cursors[part];
+        const u64* recs = B.recs + part * cap;
+        constexpr int kBatch = 2 * ETWG_PART_BATCH;  // 8-byte records: twice as many in flight
+        for (unsigned base = threadIdx.x; base < cnt; base += kBatch * blockDim.x) {
+            u64 rv[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const unsigned i = base + j * blockDim.x;
+                rv[j] = i < cnt ? __ldcs(recs + i) : ~u64{0};
+            }
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                if (rv[j] == ~u64{0}) break;
+                const unsigned low = static_cast<unsigned>(rv[j] >> 32);
+                const unsigned parent = static_cast<unsigned>(rv[j]);
+                unsigned h = (low * 0x9E3779B1u) >> (32 - 12);
+                bool placed = false;
+                for (int probe = 0; probe < 128; ++probe) {
+                    const unsigned seen = *reinterpret_cast<volatile unsigned*>(keys + h);
+                    if (seen == low) {
+                        placed = true;
+                    } else if (seen == ~0u) {
+                        const unsigned prev = atomicCAS(keys + h, ~0u, low);
+                        placed = prev == ~0u || prev == low;
+                    }
+                    if (placed) break;
+                    h = (h + 1) & (SLOTS - 1);
+                }
+                if (placed) {
+                    if (parent < *reinterpret_cast<volatile unsigned*>(ranks + h)) atomicMin(ranks + h, parent);
+                } else {
+                    s_full = 1;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_full) {
+            if (threadIdx.x == 0) {
+                C->need = 2 * np;
+                C->abort = kGrowParts;
+            }
+            return;  // block-uniform
+        }
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+            const unsigned parent = ranks[i];
+            if (parent == ~0u) continue;
+            const u64 key = unmixn((nb >= 64 ? 0 : (part << nb)) | keys[i], n);
+            if constexpr (BLOOM) {
+                const Set<1> k1 = {{key}};
+                const u64 m = bloom_bits_for(round_cap(*P, C->count[r & 1]), P->bpe);
+                const unsigned h1 = murmur_key<1>(k1, kSeed1);
+                const unsigned h2 = murmur_key<1>(k1, kSeed2);
+                u64 pos, step;
+                probe_start(h1, h2, m, pos, step);
+                atomicAdd(&C->rs[r].probed, 1ull);
+                if (!bloom_or_probes(reinterpret_cast<unsigned*>(B.bloom[r & 1]), m, pos, step, P->hashes)) {
+                    atomicAdd(&C->rs[r].fp, 1ull);
+                    if (P->flags & 2048) {
+                        const unsigned at = atomicAdd(&C->fp_log_n, 1u);
+                        if (at < 16) {
+                            C->fp_log[at][0] = key;
+                            C->fp_log[at][1] = 0;
+                            C->fp_log[at][2] = (static_cast<u64>(h1) << 32) | h2;
+                            C->fp_log[at][3] = m;
+                        }
+                    }
+                    continue;
+                }
+            }
+            const u64 bit = key & ~__ldg(layer + parent);  // the one vertex the parent lacks
+            atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + parent, bit);
         }
         if (threadIdx.x == 0) B.cursors[part] = 0;  // clean for the next round
         __syncthreads();
@@ -1032,6 +1234,7 @@ private:
         return e ? std::atoi(e) : -1;  // -1: driver default
     }();
     int grid_part_[2] = {0, 0};
+    int grid_compact_ = 0;
     bool part_bloom_ = false;  // Bloom rounds of this decide use scatter/part/append
 
     // Epochs tag look-back statuses (24 bits); on wrap-around the status
@@ -1130,7 +1333,7 @@ private:
             check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, bytes), "occupancy");
             grid = prop.multiProcessorCount * std::max(1, blocks);
         };
-        allow_exact(k_exact_scatter<1, false, false>, 0, grid_exact_[0]);
+        allow_exact(k_exact_scatter<1, false, false>, scatter_smem<1>(), grid_exact_[0]);
         allow_exact(k_exact_scatter<2, false, false>, 0, grid_exact_[1]);
         if (const char* c = std::getenv("ETWG_SCATTER_CTAS")) {  // CTAs per SM (tuning sweeps)
             const int per = std::atoi(c);
@@ -1141,7 +1344,7 @@ private:
         {
             // the Bloom variants run on the grid of their exact twin, capped by their own residency
             int g;
-            allow_exact(k_exact_scatter<1, false, true>, 0, g);
+            allow_exact(k_exact_scatter<1, false, true>, scatter_smem<1>(), g);
             grid_exact_[0] = std::min(grid_exact_[0], g);
             allow_exact(k_exact_scatter<2, false, true>, 0, g);
             grid_exact_[1] = std::min(grid_exact_[1], g);
@@ -1164,6 +1367,9 @@ private:
             int g;
             allow_part(k_exact_part<1, true>, part_smem_bytes<1>(), g);
             allow_part(k_exact_part<2, true>, part_smem_bytes<2>(), g);
+            allow_part(k_exact_part_compact<false>, compact_smem_bytes(), grid_compact_);
+            allow_part(k_exact_part_compact<true>, compact_smem_bytes(), g);
+            grid_compact_ = std::min(grid_compact_, g);
         }
         check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
         check(cudaMalloc(&d_params_, sizeof(Params)), "malloc params");
@@ -1364,10 +1570,13 @@ private:
             timed_launch([&] { k_exact_scatter<W, true, BLOOM><<<grid_exact_mmw_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
         else
-            timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
+            timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.expand_ms, prof.t.expand_launches);
         timed_launch([&] { k_exact_part<W, BLOOM><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                      prof.t.insert_ms, prof.t.insert_launches);
+        if (W == 1)  // the round's plan picks one of the two record formats; the other kernel returns at once
+            timed_launch([&] { k_exact_part_compact<BLOOM><<<grid_compact_, kPartThreads, compact_smem_bytes(), stream_>>>(d_params_, d_ctl_, b_); },
+                         prof.t.insert_ms, prof.t.insert_launches);
         timed_launch([&] { k_append<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
                      prof.t.append_ms, prof.t.append_launches);
     }
@@ -1559,9 +1768,12 @@ private:
             } else {
                 // k_exact_scatter: parent read, winner-mask clear, one record per child;
                 // k_exact_part: record read, one winner-mask OR per distinct key
-                const double rec = 8.0 * W + 8.0;
+                // (compact rounds: 8-byte records, plus the parent's set read
+                // back per distinct key)
+                const bool compact = s.round >= 0 && s.round < kMaxRounds && h_ctl_->rs[s.round].compact;
+                const double rec = compact ? 8.0 : 8.0 * W + 8.0;
                 prof.t.expand_bytes += 2 * sb * E + rec * P;
-                prof.t.insert_bytes += rec * P + 8.0 * U;
+                prof.t.insert_bytes += rec * P + (compact ? 16.0 : 8.0) * U;
             }
             // k_append: parent + history + mask read, state + history written
             prof.t.append_bytes += (sb + 4.0 + sb) * E + wb * U;

@@ -369,3 +369,13 @@ def test_partitioned_rounds_survive_aborts(gpu):
     of the record capacity) make rounds abort and re-run with raised floors;
     exact layers, orders, histories and counters are unchanged."""
     assert _run_with_debug(1024, _TIGHT_CODE) == _run_with_debug(0, _TIGHT_CODE)
+
+
+def test_compact_and_wide_records_agree(gpu):
+    """ETWG_DEBUG 4096 forces the 16-byte {key, rank} records on every round;
+    by default rounds of one-word keys use 8-byte {mixed-key bits, parent}
+    records (PartPlan, wavefront.cu). Layers, histories and counters must
+    not depend on the format, including under the tight plans' aborts."""
+    wide = _run_with_debug(4096, _TIGHT_CODE)
+    assert wide == _run_with_debug(0, _TIGHT_CODE)
+    assert wide == _run_with_debug(1024 | 4096, _TIGHT_CODE)

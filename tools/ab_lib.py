@@ -23,8 +23,13 @@ print(json.dumps({"g48": sorted(ts), "stats": r.stats_json, "queen": [tq, rq.sta
 reps = sys.argv[3] if len(sys.argv) > 3 else "3"
 dedup = sys.argv[4] if len(sys.argv) > 4 else "exact"
 outs = []
-for lib in sys.argv[1:3]:
+for spec in sys.argv[1:3]:
+    # "path.so" or "path.so@VAR=value,VAR2=value" (extra environment for that run)
+    lib, _, extra = spec.partition("@")
     env = dict(os.environ, ETWG_LIB=os.path.abspath(lib))
+    for kv in filter(None, extra.split(",")):
+        k, v = kv.split("=", 1)
+        env[k] = v
     p = subprocess.run([sys.executable, "-c", CODE, reps, dedup], env=env, capture_output=True, text=True, timeout=900)
     if p.returncode:
         print(lib, "failed", p.stderr[-2000:]); sys.exit(1)
