@@ -514,6 +514,93 @@ __device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, con
 constexpr int kSigComps = ETWG_SIG_COMPS;
 constexpr int sig_smem_bytes(int threads) { return threads * (kSigComps * 8 + 64 * 2); }
 
+// K1 for one-word keys with every relevant component in a register slot
+// (isolated members too: their boundary is their row), held as 32-bit halves.
+// The candidate loop runs once over the low and once over the high half of
+// the candidate mask, so a candidate's bit lies in a known half: testing
+// whether v touches a component is one AND on that half of its boundary,
+// and the whole test costs ~3 instructions per slot, no inner loop.
+// Components beyond kHalfSlots go to a local array walked with a
+// loop-uniform index (rare: stats in DESIGN.md §4).
+#ifndef ETWG_HALF_SLOTS
+#define ETWG_HALF_SLOTS 8
+#endif
+constexpr int kHalfSlots = ETWG_HALF_SLOTS;
+
+__device__ __forceinline__ u64 candidates_half(const Set<1>* adj, int k, u64 S, u64 eligible) {
+    unsigned slo[kHalfSlots], shi[kHalfSlots];
+#pragma unroll
+    for (int j = 0; j < kHalfSlots; ++j) slo[j] = shi[j] = 0;
+    u64 spill[32];
+    int ns = 0;
+    u64 reject = 0;
+    u64 rem = S, frontier = 0, nb = 0, comp = 0;
+    const int r = __popcll(S);
+    for (int it = 0; it < r; ++it) {
+        if (!frontier) {
+            frontier = u64{1} << (63 - __clzll(rem));
+            rem ^= frontier;
+            comp = frontier;
+            nb = 0;
+        }
+        const int x = 63 - __clzll(frontier);
+        frontier ^= u64{1} << x;
+        const u64 a = adj[x].w[0];
+        nb |= a;
+        const u64 fresh = a & rem;
+        rem ^= fresh;
+        comp |= fresh;
+        frontier |= fresh;
+        if (frontier) continue;
+        const u64 B = nb & ~S;
+        if (!(B & eligible)) continue;
+        if (__popcll(B) > k + 1) {
+            reject |= B;
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < kHalfSlots; ++j)
+            if (ns == j) {
+                slo[j] = static_cast<unsigned>(B);
+                shi[j] = static_cast<unsigned>(B >> 32);
+            }
+        if (ns >= kHalfSlots) spill[ns - kHalfSlots] = B;
+        ++ns;
+    }
+    const u64 cand = eligible & ~reject;
+    const unsigned Slo = static_cast<unsigned>(S), Shi = static_cast<unsigned>(S >> 32);
+    u64 keep = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        unsigned y = static_cast<unsigned>(cand >> (32 * h));
+        while (y) {
+            const int b = 31 - __clz(y);
+            const unsigned bit = 1u << b;
+            y ^= bit;
+            const int v = 32 * h + b;
+            const u64 a = adj[v].w[0];
+            unsigned qlo = static_cast<unsigned>(a) & ~Slo, qhi = static_cast<unsigned>(a >> 32) & ~Shi;
+#pragma unroll
+            for (int j = 0; j < kHalfSlots; ++j) {
+                if (((h ? shi[j] : slo[j]) & bit) != 0) {
+                    qlo |= slo[j];
+                    qhi |= shi[j];
+                }
+            }
+            for (int j = kHalfSlots; j < ns; ++j) {
+                const u64 Bj = spill[j - kHalfSlots];
+                if ((Bj >> v) & 1) {
+                    qlo |= static_cast<unsigned>(Bj);
+                    qhi |= static_cast<unsigned>(Bj >> 32);
+                }
+            }
+            if (h) qhi &= ~bit; else qlo &= ~bit;
+            if (__popc(qlo) + __popc(qhi) <= k) keep |= u64{1} << v;
+        }
+    }
+    return keep;
+}
+
 // the rare overflow path of candidates_sig, out of line so its registers
 // do not count against the common path
 __device__ __noinline__ u64 candidates_slots_w1(const Set<1>* adj, int k, u64 S, u64 eligible) {
@@ -625,11 +712,15 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
     Set<W> keep = Set<W>::zero();
     if (eligible.none()) return keep;
     if constexpr (!MMW) {
-        if (ETWG_K1 == 2) return candidates_slots<W>(adj, k, S, eligible);
+        if constexpr (W == 1 && ETWG_K1 == 4) {
+            keep.w[0] = candidates_half(adj, k, S.w[0], eligible.w[0]);
+            return keep;
+        }
+        if (ETWG_K1 >= 2) return candidates_slots<W>(adj, k, S, eligible);
         if (Rsh && S.count() <= kShSlots) return candidates_shared<W>(adj, k, S, eligible, Rsh);
     }
     Set<W> R[N];
-    if (ETWG_K1 != 2) component_reach<W, COMPACT>(adj, S, R);
+    if (ETWG_K1 < 2) component_reach<W, COMPACT>(adj, S, R);
     if constexpr (!MMW) {
         for_each_any(eligible, [&](int v) {
             if ((adj[v] - S).count() > k) return;  // |Q(S,v)| >= |N(v) \ S|
@@ -637,7 +728,7 @@ __device__ __forceinline__ Set<W> candidates(const Set<W>* adj, int n, int k, co
         });
     } else {
         Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
-        if (ETWG_K1 == 2)
+        if (ETWG_K1 >= 2)
             q_rows<W>(adj, S, open, rows);
         else
             for (int w : members(open)) rows[w] = reach_from<W, COMPACT>(adj, S, R, w);
@@ -686,7 +777,7 @@ __device__ __forceinline__ Set<W> warp_candidates(const Set<W>* adj, int n, int 
             if (j < f.total) {
                 const int v = nth_member<W>(Ms, j - excl);
                 Set<W> rows[N];  // dp.cpp:51-53: Q(S,w) for every open w
-                if (ETWG_K1 == 2) {
+                if (ETWG_K1 >= 2) {
                     q_rows<W>(adj, Ss, Set<W>::prefix(n) - Ss, rows);
                 } else {
                     Set<W> R[N];
@@ -724,7 +815,7 @@ __device__ __forceinline__ Set<W> warp_parent_candidates(const Set<W>* adj, int 
     const Set<W> open = Set<W>::prefix(n) - S;
     const Set<W> eligible = open - forbidden;
     if (eligible.none()) return Set<W>::zero();
-#if ETWG_K1 == 2
+#if ETWG_K1 >= 2
     // S is warp-uniform: every lane builds the same component list (no
     // serial lane-0 fill, no shared table)
     Comps<W> c;
@@ -741,7 +832,7 @@ __device__ __forceinline__ Set<W> warp_parent_candidates(const Set<W>* adj, int 
             const int v = nth_member<W>(eligible, i);
             const Set<W> q0 = adj[v] - S;
             if (q0.count() > k) continue;
-#if ETWG_K1 == 2
+#if ETWG_K1 >= 2
             if (!c.reject.has(v) && c.q(adj, adj[v], q0, v, spill).count() <= k) mine.add(v);
 #else
             if (reach_from<W, false>(adj, S, R, v).count() <= k) mine.add(v);
@@ -751,7 +842,7 @@ __device__ __forceinline__ Set<W> warp_parent_candidates(const Set<W>* adj, int 
         const int no = open.count();
         for (int i = lane; i < no; i += 32) {  // dp.cpp:51-53: Q(S,w) for every open w
             const int w = nth_member<W>(open, i);
-#if ETWG_K1 == 2
+#if ETWG_K1 >= 2
             rows[w] = c.q(adj, S, w, spill);
 #else
             rows[w] = reach_from<W, false>(adj, S, R, w);

@@ -140,7 +140,10 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #define ETWG_APPEND_MINB 4  // k_append: >= 4 resident CTAs per SM (registers <= 64)
 #endif
 #ifndef ETWG_EMIT_FLAT
-#define ETWG_EMIT_FLAT 1  // 1: children flattened over the warp's lanes; 0: each lane emits its own
+#define ETWG_EMIT_FLAT 0  // 1: children flattened over the warp's lanes; 0: each lane emits its own (-0.8 %)
+#endif
+#ifndef ETWG_COMPACT
+#define ETWG_COMPACT 0  // 1: 8-byte records on every eligible round (see PartPlan)
 #endif
 #ifndef ETWG_EMIT_UNROLL
 #define ETWG_EMIT_UNROLL 2  // children emitted per lane per step in k_exact_scatter
@@ -242,7 +245,11 @@ __device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C,
     while ((u64{1} << pl.lg) < pl.np) ++pl.lg;
     pl.compact = 0;
     pl.nb = 0;
-    if (W == 1 && !(P->flags & 4096) && E <= 0xFFFFFFFFull) {  // ETWG_DEBUG 4096: 16-byte records only
+    // compact records: ETWG_COMPACT=1 at build time or ETWG_DEBUG 8192; off by
+    // default (measured on G(48,0.2): 1.054 s vs 1.033 s with 16-byte records —
+    // the per-distinct-key read of the parent set costs more than the halved
+    // record traffic saves)
+    if (W == 1 && (ETWG_COMPACT || (P->flags & 8192)) && E <= 0xFFFFFFFFull) {
         // up to 4x the planned buckets to bring the record's key bits to 31
         const int need = P->n - 31 > pl.lg ? P->n - 31 : pl.lg;
         if (need - pl.lg <= 2) {

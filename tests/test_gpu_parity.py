@@ -372,10 +372,10 @@ def test_partitioned_rounds_survive_aborts(gpu):
 
 
 def test_compact_and_wide_records_agree(gpu):
-    """ETWG_DEBUG 4096 forces the 16-byte {key, rank} records on every round;
-    by default rounds of one-word keys use 8-byte {mixed-key bits, parent}
-    records (PartPlan, wavefront.cu). Layers, histories and counters must
-    not depend on the format, including under the tight plans' aborts."""
-    wide = _run_with_debug(4096, _TIGHT_CODE)
-    assert wide == _run_with_debug(0, _TIGHT_CODE)
-    assert wide == _run_with_debug(1024 | 4096, _TIGHT_CODE)
+    """ETWG_DEBUG 8192 turns on the 8-byte {mixed-key bits, parent} records
+    for rounds of one-word keys (PartPlan, wavefront.cu; the default is the
+    16-byte {key, rank} record). Layers, histories and counters must not
+    depend on the format, including under the tight plans' aborts."""
+    wide = _run_with_debug(0, _TIGHT_CODE)
+    assert wide == _run_with_debug(8192, _TIGHT_CODE)
+    assert wide == _run_with_debug(1024 | 8192, _TIGHT_CODE)
