@@ -270,13 +270,15 @@ def roofline(p):
     # DRAM traffic from the committed ncu --set full capture of this kernel's
     # longest launch (tools/ncu_traffic.py), scaled to the average launch
     traffic, traffic_src, alu = None, None, None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             tr = json.load(f).get(name)
         if tr:
             traffic = tr["traffic_over_algorithmic"] * per_launch
-            traffic_src = (f"profiles/r01_traffic.json: ncu --set full of the longest launch, DRAM bytes = "
+            traffic_src = (f"{os.path.relpath(tpath, ROOT)}: ncu --set full of the longest launch, DRAM bytes = "
                            f"{tr['traffic_over_algorithmic']:.2f} x algorithmic bytes, scaled to the average launch")
             if "issue_slots_busy_pct" in tr:
                 alu = {"bound": "integer ALU issue", "issue_slots_busy_pct": tr["issue_slots_busy_pct"],

@@ -382,7 +382,7 @@ __device__ __forceinline__ Set<W> candidates_shared(const Set<W>* adj, int k, co
 // number, the same for every lane), and the candidate loop runs over the
 // eligible set, whose size n - |S| - |forbidden| is also warp-uniform.
 #ifndef ETWG_K1
-#define ETWG_K1 2  // 2: register boundary slots; 1: per-vertex table (component_reach)
+#define ETWG_K1 4  // 4: half-word register slots (one-word keys); 2: register slots + isolated-member loop; 3: shared signatures; 1: per-vertex table
 #endif
 #ifndef ETWG_K1_LOOP
 #define ETWG_K1_LOOP 2  // 1: two 32-bit half loops with an early |N(v) \ S| > k exit
