@@ -88,6 +88,8 @@ struct Control {
     unsigned handed, pad2;
     u64 part_floor;     // exact mode: minimum partitions after a grow (per decide)
     u64 rec_floor;      // exact mode: minimum records per partition after a grow
+    unsigned passes;    // exact mode: hash-range passes per round (host-set, >= 1)
+    unsigned pass;      // current pass of the round (k_pass_advance; reset by the append)
     unsigned fp_log_n;  // ETWG_DEBUG 2048: first false positives logged (key, h1, h2, m)
     unsigned pad3;
     u64 fp_log[16][4];
@@ -223,6 +225,13 @@ struct PartPlan {
     int lg;
     int compact;  // 8-byte records this round
     int nb;       // bits of the mixed key a compact record carries (n - lg)
+    // Hash-range passes (records beyond HBM): pass p of `passes` handles the
+    // buckets with part % passes == p; K1 reruns per pass, records of one
+    // pass only are held, so the record buffer is np/passes * cap.
+    unsigned passes, pass;
+    int lgp;  // log2(passes)
+    __device__ __forceinline__ bool mine(u64 part) const { return (part & (passes - 1)) == pass; }
+    __device__ __forceinline__ u64 local(u64 part) const { return part >> lgp; }
 };
 
 template <int W>
@@ -259,6 +268,14 @@ __device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C,
             pl.nb = P->n - pl.lg;
         }
     }
+    pl.passes = C->passes ? C->passes : 1;
+    pl.pass = C->pass;
+    if (pl.np < pl.passes) {
+        pl.lg += __ffs(static_cast<int>(pl.passes)) - 1 - (__ffsll(static_cast<long long>(pl.np)) - 1);
+        pl.np = pl.passes;
+        if (pl.compact) pl.nb = P->n - pl.lg;
+    }
+    pl.lgp = __ffs(static_cast<int>(pl.passes)) - 1;
     const u64 per = (winners + pl.np - 1) / pl.np;
     pl.cap = tight ? per / 4 + 1 : per + per / 4 + 64;
     if (pl.cap < C->rec_floor) pl.cap = C->rec_floor;
@@ -285,11 +302,12 @@ __device__ __forceinline__ u64 record_part(const Set<W>& key, const PartPlan& pl
 template <int W>
 __device__ __forceinline__ void record_store(const Bufs& B, const PartPlan& pl, u64 part, unsigned slot,
                                              const Set<W>& key, u64 low, u64 parent, int v) {
+    const u64 lp = pl.local(part);
     if (W == 1 && pl.compact) {
-        B.recs[part * pl.cap + slot] = (low << 32) | parent;
+        B.recs[lp * pl.cap + slot] = (low << 32) | parent;
         return;
     }
-    u64* rec = B.recs + (part * pl.cap + slot) * rec_words<W>();
+    u64* rec = B.recs + (lp * pl.cap + slot) * rec_words<W>();
     if constexpr (W == 1) {
         *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(parent, v));
     } else {
@@ -322,9 +340,10 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
     const PartPlan pl = part_plan<W>(P, C, r, E);
-    if (pl.np > B.cursor_cap || pl.np * pl.cap > B.rec_cap) {
+    const u64 rec_need = (pl.np >> pl.lgp) * pl.cap * (W == 1 && pl.compact ? 1 : rec_words<W>());  // u64 words
+    if (pl.np > B.cursor_cap || rec_need > B.rec_cap) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            C->need = pl.np * pl.cap;
+            C->need = rec_need;
             C->abort = kGrowPartBuf;
         }
         return;
@@ -341,7 +360,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
             }
             return;
         }
-        if (r > 0) {
+        if (r > 0 && pl.pass == 0) {
             const u64 gtid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
             const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
             const u64 prev_words = bloom_bits_for(round_cap(*P, C->rs[r - 1].expanded), P->bpe) / 32 + 1;
@@ -381,7 +400,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
             const Set<W> S = load_set<W>(in, p);
             const Set<W> M = warp_parent_candidates<W, MMW>(adj, P->n, P->k, S, forbidden, pruned, R, rows);
             const int cnt = M.count();
-            if (lane == 0) {
+            if (lane == 0 && pl.pass == 0) {  // counters and mask clear once per round, not per pass
                 offered += cnt;
                 winners += cnt;
                 store_set<W>(B.cmask, p, Set<W>::zero());
@@ -392,6 +411,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 key.add(v);
                 u64 low;
                 const u64 part = record_part<W>(key, pl, n, low);
+                if (!pl.mine(part)) continue;
                 const unsigned slot = atomicAdd(B.cursors + part, 1u);
                 if (slot < pl.cap)
                     record_store<W>(B, pl, part, slot, key, low, p, v);
@@ -420,9 +440,11 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         } else {
             M = warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         }
-        offered += M.count();
-        winners += M.count();
-        if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
+        if (pl.pass == 0) {  // counters and mask clear once per round, not per pass
+            offered += M.count();
+            winners += M.count();
+            if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
+        }
         bool full = false;
 #if ETWG_EMIT_FLAT == 0
         // each lane emits its own parent's children, two per step so both
@@ -442,7 +464,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                     key[u] = S;
                     key[u].add(vv[u]);
                     part[u] = record_part<W>(key[u], pl, n, low[u]);
-                    slot[u] = atomicAdd(B.cursors + part[u], 1u);
+                    if (pl.mine(part[u])) slot[u] = atomicAdd(B.cursors + part[u], 1u);
                 }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
@@ -478,7 +500,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                     vv[u] = nth_member<W>(Ms, j - excl);
                     key[u].add(vv[u]);
                     part[u] = record_part<W>(key[u], pl, n, low[u]);
-                    slot[u] = atomicAdd(B.cursors + part[u], 1u);
+                    if (pl.mine(part[u])) slot[u] = atomicAdd(B.cursors + part[u], 1u);
                 }
             }
 #pragma unroll
@@ -504,9 +526,15 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     }
     if (lane == 0) {
         if (offered) atomicAdd(&C->rs[r].offered, offered);
-        if (pruned) atomicAdd(&C->rs[r].mmw_pruned, pruned);
+        if (pruned && pl.pass == 0) atomicAdd(&C->rs[r].mmw_pruned, pruned);
         if (winners) atomicAdd(&C->rs[r].winners, winners);
     }
+}
+
+// pass p of a hash-range-partitioned round is done: the next scatter / part
+// pair takes pass p+1 (the round's append resets it)
+__global__ void k_pass_advance(Control* C) {
+    if (!halted(C)) C->pass += 1;
 }
 
 constexpr int kPartThreads = 512;
@@ -529,15 +557,18 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
     if (halted(C)) return;
     const unsigned r = C->round;
     if (W == 1 && C->rs[r].compact) return;  // k_exact_part_compact's round
-    const u64 np = C->rs[r].np;
+    const u64 passes = C->passes ? C->passes : 1;
+    const u64 pass = C->pass;
+    const u64 np = C->rs[r].np / passes;  // this pass's buckets: part = lp * passes + pass
     const u64 cap = C->rs[r].pcap;
-    for (u64 part = blockIdx.x; part < np; part += gridDim.x) {
+    for (u64 lp = blockIdx.x; lp < np; lp += gridDim.x) {
+        const u64 part = lp * passes + pass;
         for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) keys[i] = 0;
         for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) ranks[i] = ~u64{0};
         if (threadIdx.x == 0) s_full = 0;
         __syncthreads();
         const unsigned cnt = B.cursors[part];
-        const u64* recs = B.recs + part * cap * rec_words<W>();
+        const u64* recs = B.recs + lp * cap * rec_words<W>();
         // PART_BATCH records in flight per thread before any probing: one
         // outstanding 16 B load per thread cannot cover HBM latency at the
         // 3 CTAs/SM the 64 KB tables allow
@@ -581,7 +612,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
         __syncthreads();
         if (s_full) {
             if (threadIdx.x == 0) {
-                C->need = 2 * np;
+                C->need = 2 * np * passes;
                 C->abort = kGrowParts;
             }
             return;  // block-uniform
@@ -642,12 +673,15 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Param
     if (halted(C)) return;
     const unsigned r = C->round;
     if (!C->rs[r].compact) return;
-    const u64 np = C->rs[r].np;
+    const u64 passes = C->passes ? C->passes : 1;
+    const u64 pass = C->pass;
+    const u64 np = C->rs[r].np / passes;
     const u64 cap = C->rs[r].pcap;
     const int nb = static_cast<int>(C->rs[r].nb);
     const int n = P->n;
     const u64* layer = B.keys[r & 1];
-    for (u64 part = blockIdx.x; part < np; part += gridDim.x) {
+    for (u64 lp = blockIdx.x; lp < np; lp += gridDim.x) {
+        const u64 part = lp * passes + pass;
         for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
             keys[i] = ~0u;
             ranks[i] = ~0u;
@@ -655,7 +689,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Param
         if (threadIdx.x == 0) s_full = 0;
         __syncthreads();
         const unsigned cnt = B.cursors[part];
-        const u64* recs = B.recs + part * cap;
+        const u64* recs = B.recs + lp * cap;
         constexpr int kBatch = 2 * ETWG_PART_BATCH;  // 8-byte records: twice as many in flight
         for (unsigned base = threadIdx.x; base < cnt; base += kBatch * blockDim.x) {
             u64 rv[kBatch];
@@ -692,7 +726,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Param
         __syncthreads();
         if (s_full) {
             if (threadIdx.x == 0) {
-                C->need = 2 * np;
+                C->need = 2 * np * passes;
                 C->abort = kGrowParts;
             }
             return;  // block-uniform
@@ -924,6 +958,7 @@ __device__ __forceinline__ void finish_round(const Params* P, Control* C, const 
     rs.valid = 1;
     C->count[(r + 1) & 1] = emitted;
     C->round = r + 1;
+    C->pass = 0;
     C->epoch = (C->epoch & kEpochMask) == kEpochMask ? 1 : C->epoch + 1;
     if (emitted == 0 || static_cast<int>(r) + 1 >= P->rounds) {
         C->stop = 1;
@@ -1242,6 +1277,8 @@ private:
     }();
     int grid_part_[2] = {0, 0};
     int grid_compact_ = 0;
+    bool compact_possible_ = false;  // ETWG_COMPACT build or ETWG_DEBUG 8192 this decide
+    unsigned passes_ = 1;            // hash-range passes per round (f4: records beyond HBM)
     bool part_bloom_ = false;  // Bloom rounds of this decide use scatter/part/append
 
     // Epochs tag look-back statuses (24 bits); on wrap-around the status
@@ -1426,6 +1463,14 @@ private:
         c.count[0] = first_count;
         c.handoff_above = handoff_above;
         c.epoch = next_epoch();
+        // ETWG_PASSES: minimum hash-range passes per round (a power of two;
+        // tests / out-of-HBM rehearsal); the engine doubles it when the child
+        // records of a round do not fit the device
+        passes_ = 1;
+        if (const char* e = std::getenv("ETWG_PASSES"))
+            while (passes_ < 1024 && passes_ * 2 <= static_cast<unsigned>(std::max(1, std::atoi(e)))) passes_ *= 2;
+        c.passes = passes_;
+        compact_possible_ = ETWG_COMPACT || (h_params_->flags & 8192);
         copy(d_ctl_, h_ctl_, sizeof(Control), cudaMemcpyHostToDevice, "control");
     }
 
@@ -1466,11 +1511,21 @@ private:
 
     // Exact-mode record buckets; cursors start (and are left by every
     // completed round) at zero.
-    void ensure_parts(u64 recs, u64 parts) {
-        if (recs > b_.rec_cap || !b_.recs) {
-            const u64 cap = std::max<u64>(recs, u64{1} << 20);
+    // records: `words` u64 words (2 per 16-byte record, 4 per 32-byte, 1 per
+    // compact); false when the device cannot hold them (the caller then
+    // splits the round into more hash-range passes)
+    bool ensure_parts(u64 words, u64 parts) {
+        if (words > b_.rec_cap || !b_.recs) {
+            const u64 cap = std::max<u64>(words, u64{1} << 21);
             if (b_.recs) cudaFree(b_.recs);
-            check(cudaMalloc(&b_.recs, cap * 32), "records");
+            b_.recs = nullptr;
+            b_.rec_cap = 0;
+            const cudaError_t e = cudaMalloc(&b_.recs, cap * 8);
+            if (e == cudaErrorMemoryAllocation && words > (u64{1} << 21)) {
+                cudaGetLastError();
+                return false;
+            }
+            check(e, "records");
             b_.rec_cap = cap;
         }
         if (parts > b_.cursor_cap || !b_.cursors) {
@@ -1480,6 +1535,7 @@ private:
             check(cudaMemsetAsync(b_.cursors, 0, cap * 4, stream_), "cursors zero");
             b_.cursor_cap = cap;
         }
+        return true;
     }
 
     void clean_cursors() {
@@ -1573,17 +1629,23 @@ private:
     template <int W, bool BLOOM, typename Launch>
     void launch_partitioned(const DpConfig& cfg, Launch&& timed_launch) {
         const int smem = 0;
-        if (cfg.use_mmw)
-            timed_launch([&] { k_exact_scatter<W, true, BLOOM><<<grid_exact_mmw_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
-                         prof.t.expand_ms, prof.t.expand_launches);
-        else
-            timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
-                         prof.t.expand_ms, prof.t.expand_launches);
-        timed_launch([&] { k_exact_part<W, BLOOM><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
-                     prof.t.insert_ms, prof.t.insert_launches);
-        if (W == 1)  // the round's plan picks one of the two record formats; the other kernel returns at once
-            timed_launch([&] { k_exact_part_compact<BLOOM><<<grid_compact_, kPartThreads, compact_smem_bytes(), stream_>>>(d_params_, d_ctl_, b_); },
+        for (unsigned pass = 0; pass < passes_; ++pass) {
+            if (cfg.use_mmw)
+                timed_launch([&] { k_exact_scatter<W, true, BLOOM><<<grid_exact_mmw_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.expand_ms, prof.t.expand_launches);
+            else
+                timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.expand_ms, prof.t.expand_launches);
+            timed_launch([&] { k_exact_part<W, BLOOM><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                          prof.t.insert_ms, prof.t.insert_launches);
+            if (W == 1 && compact_possible_)  // the plan picks one record format; the other kernel returns at once
+                timed_launch([&] { k_exact_part_compact<BLOOM><<<grid_compact_, kPartThreads, compact_smem_bytes(), stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.insert_ms, prof.t.insert_launches);
+            if (passes_ > 1) {
+                k_pass_advance<<<1, 1, 0, stream_>>>(d_ctl_);
+                check(cudaGetLastError(), "pass advance");
+            }
+        }
         timed_launch([&] { k_append<W><<<grid_, kThreads, 0, stream_>>>(d_params_, d_ctl_, b_); },
                      prof.t.append_ms, prof.t.append_launches);
     }
@@ -1602,7 +1664,7 @@ private:
     }
 
     void run_rounds(int W, const DpConfig& cfg, int rounds, int k, const LayerObserver* observer) {
-        ensure_parts(u64{1} << 20, u64{1} << 22);
+        if (!ensure_parts(u64{1} << 21, u64{1} << 22)) throw DeviceError("device engine: no memory for records");
         ensure_bloom(u64{1} << 22);
         ensure_claims(u64{1} << 20);
         bloom_round_ = cfg.dedup == DedupMode::bloom;
@@ -1704,7 +1766,16 @@ private:
                 clean_cursors();
                 break;
             case kGrowPartBuf:
-                ensure_parts(c.need + c.need / 4, 0);
+                // f4: child records beyond HBM -> twice the hash-range passes
+                // per round (K1 reruns per pass; same layers, same counters)
+                while (!ensure_parts(c.need + c.need / 4, 0)) {
+                    if (passes_ >= 1024) throw DeviceError("device engine: child records exceed device memory");
+                    passes_ *= 2;
+                    c.passes = passes_;
+                    c.need = (c.need + 1) / 2;
+                    if (std::getenv("ETWG_TRACE"))
+                        std::fprintf(stderr, "[engine] records do not fit: %u hash-range passes per round\n", passes_);
+                }
                 clean_cursors();
                 break;
             case kGrowBloom:
@@ -1721,6 +1792,7 @@ private:
         c.abort = kOk;
         c.need = 0;
         c.exits = 0;
+        c.pass = 0;
         c.epoch = next_epoch();  // statuses of the aborted attempt must not match
         std::memset(&c.rs[r], 0, sizeof(RoundStats) * (kMaxRounds - r));
         copy(d_ctl_, h_ctl_, sizeof(Control), cudaMemcpyHostToDevice, "control re-arm");

@@ -311,6 +311,29 @@ def test_partitioned_bloom_large_filter(E, gpu):
     assert res.value == 22
 
 
+def _run_with_env(env_extra, code):
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, **env_extra)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def test_hash_range_passes_agree(gpu):
+    """f4 (out-of-HBM child records): with ETWG_PASSES=P every exact round
+    runs as P hash-range passes (K1 reruns per pass, each pass dedups and
+    marks only its buckets, the append runs once). Layers, histories and
+    counters are identical to the one-pass rounds, also under aborts."""
+    one = _run_with_env({}, _TIGHT_CODE)
+    assert one == _run_with_env({"ETWG_PASSES": "4"}, _TIGHT_CODE)
+    assert one == _run_with_env({"ETWG_PASSES": "8", "ETWG_DEBUG": "1024"}, _TIGHT_CODE)
+    assert one == _run_with_env({"ETWG_PASSES": "2", "ETWG_DEBUG": "8192"}, _TIGHT_CODE)
+
+
 def _run_with_debug(flags, code):
     """Runs `code` in a fresh interpreter with ETWG_DEBUG=flags (the engine
     reads it when a decide starts) and returns its JSON output."""
