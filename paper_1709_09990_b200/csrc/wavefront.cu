@@ -144,6 +144,12 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_EMIT_FLAT
 #define ETWG_EMIT_FLAT 0  // 1: children flattened over the warp's lanes; 0: each lane emits its own (-0.8 %)
 #endif
+#ifndef ETWG_LANE_UNROLL
+#define ETWG_LANE_UNROLL 2  // children per lane whose bucket-cursor atomics are in flight together
+#endif
+#ifndef ETWG_REC_EVICT_LAST
+#define ETWG_REC_EVICT_LAST 0  // 1: child records stored with an L2 evict-last hint
+#endif
 #ifndef ETWG_COMPACT
 #define ETWG_COMPACT 0  // 1: 8-byte records on every eligible round (see PartPlan)
 #endif
@@ -309,7 +315,18 @@ __device__ __forceinline__ void record_store(const Bufs& B, const PartPlan& pl, 
     }
     u64* rec = B.recs + (lp * pl.cap + slot) * rec_words<W>();
     if constexpr (W == 1) {
+#if ETWG_REC_EVICT_LAST
+        // keep the bucket tails in L2 until both halves of each 32-byte
+        // sector are written (a partial sector evicted costs a DRAM
+        // read-modify-write)
+        u64 pol;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(rec), "l"(key.w[0]),
+                     "l"(child_rank<W>(parent, v)), "l"(pol)
+                     : "memory");
+#else
         *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(parent, v));
+#endif
     } else {
         *reinterpret_cast<ulonglong4*>(rec) = make_ulonglong4(key.w[0], key.w[1], child_rank<W>(parent, v), 0);
     }
@@ -452,13 +469,16 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         // shuffles (the trip count is the warp's largest child count)
         {
             Set<W> rest = M;
+            constexpr int LU = ETWG_LANE_UNROLL;
             while (rest.any()) {
-                Set<W> key[2];
-                u64 part[2], low[2];
-                int vv[2];
-                unsigned slot[2] = {~0u, ~0u};
+                Set<W> key[LU];
+                u64 part[LU], low[LU];
+                int vv[LU];
+                unsigned slot[LU];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < LU; ++u) slot[u] = ~0u;
+#pragma unroll
+                for (int u = 0; u < LU; ++u) {
                     if (!rest.any()) break;
                     vv[u] = pop_any(rest);
                     key[u] = S;
@@ -467,7 +487,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                     if (pl.mine(part[u])) slot[u] = atomicAdd(B.cursors + part[u], 1u);
                 }
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < LU; ++u) {
                     if (slot[u] == ~0u) continue;
                     if (slot[u] < pl.cap)
                         record_store<W>(B, pl, part[u], slot[u], key[u], low[u], idx, vv[u]);
@@ -561,6 +581,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
     const u64 pass = C->pass;
     const u64 np = C->rs[r].np / passes;  // this pass's buckets: part = lp * passes + pass
     const u64 cap = C->rs[r].pcap;
+    u64 probed = 0;  // BLOOM: distinct keys sent through the filter (one atomic per thread at exit)
     for (u64 lp = blockIdx.x; lp < np; lp += gridDim.x) {
         const u64 part = lp * passes + pass;
         for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) keys[i] = 0;
@@ -631,7 +652,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
                 const unsigned h2 = murmur_key<W>(key, kSeed2);
                 u64 pos, step;
                 probe_start(h1, h2, m, pos, step);
-                atomicAdd(&C->rs[r].probed, 1ull);
+                ++probed;
                 if (!bloom_or_probes(bits, m, pos, step, P->hashes)) {
                     // a distinct key of the round whose probe bits were all set
                     // by other keys: a false positive (the reference drops it too)
@@ -654,6 +675,11 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
         }
         if (threadIdx.x == 0) B.cursors[part] = 0;  // clean for the next round
         __syncthreads();
+    }
+    if (BLOOM) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) probed += __shfl_xor_sync(kFull, probed, o);
+        if ((threadIdx.x & 31) == 0 && probed) atomicAdd(&C->rs[r].probed, probed);
     }
 }
 
@@ -678,6 +704,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Param
     const u64 np = C->rs[r].np / passes;
     const u64 cap = C->rs[r].pcap;
     const int nb = static_cast<int>(C->rs[r].nb);
+    u64 probed = 0;
     const int n = P->n;
     const u64* layer = B.keys[r & 1];
     for (u64 lp = blockIdx.x; lp < np; lp += gridDim.x) {
@@ -742,7 +769,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Param
                 const unsigned h2 = murmur_key<1>(k1, kSeed2);
                 u64 pos, step;
                 probe_start(h1, h2, m, pos, step);
-                atomicAdd(&C->rs[r].probed, 1ull);
+                ++probed;
                 if (!bloom_or_probes(reinterpret_cast<unsigned*>(B.bloom[r & 1]), m, pos, step, P->hashes)) {
                     atomicAdd(&C->rs[r].fp, 1ull);
                     if (P->flags & 2048) {
@@ -762,6 +789,11 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Param
         }
         if (threadIdx.x == 0) B.cursors[part] = 0;  // clean for the next round
         __syncthreads();
+    }
+    if (BLOOM) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) probed += __shfl_xor_sync(kFull, probed, o);
+        if ((threadIdx.x & 31) == 0 && probed) atomicAdd(&C->rs[r].probed, probed);
     }
 }
 
