@@ -1,5 +1,6 @@
 // Minor-min-width contraction loop shared by the host (one-off root bound,
-// solver.cpp:31) and the device prune (wavefront.cu k_expand). Restates
+// solver.cpp:31) and the oracle-parity MMW traces; the device prune runs
+// mmw_child (wave_device.cuh) on an explicit minor instead. Restates
 // run_mmw / contract_step / adjacent_roots (proj/src/mmw.cpp:49-140) over a
 // byte-per-vertex DSU and degree array, walking the original graph through
 // eliminated vertices and same-class members instead of building the minor.

@@ -144,6 +144,13 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_EMIT_FLAT
 #define ETWG_EMIT_FLAT 0  // 1: children flattened over the warp's lanes; 0: each lane emits its own (-0.8 %)
 #endif
+#ifndef ETWG_WARP_DEDUP
+#define ETWG_WARP_DEDUP 0  // 1: warp-private pre-dedup of children before the bucket scatter
+#endif
+#ifndef ETWG_DD_SLOTS
+#define ETWG_DD_SLOTS 512
+#endif
+constexpr int kDDSlots = ETWG_DD_SLOTS;
 #ifndef ETWG_LANE_UNROLL
 #define ETWG_LANE_UNROLL 2  // children per lane whose bucket-cursor atomics are in flight together
 #endif
@@ -352,6 +359,9 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     extern __shared__ __align__(16) unsigned char scatter_dyn[];
     u64* sig_bs = reinterpret_cast<u64*>(scatter_dyn);
     unsigned short* sig_tab = reinterpret_cast<unsigned short*>(sig_bs + kSigComps * kThreads);
+    // ETWG_WARP_DEDUP: per-warp {key, min local rank} tables (same dynamic block)
+    u64* dd_keys = reinterpret_cast<u64*>(scatter_dyn);
+    unsigned* dd_rank = reinterpret_cast<unsigned*>(dd_keys + kDDSlots * (kThreads / 32));
     __shared__ Set<W> warp_tables[kThreads / 32][MMW ? 2 : 1][64 * W];  // small-layer mode
     if (halted(C)) return;
     const unsigned r = C->round;
@@ -400,6 +410,11 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     load_adjacency<W>(P, adj);
     if constexpr (W == 1 && !MMW && ETWG_K1 == 3)
         for (int i = threadIdx.x; i < 64 * kThreads; i += blockDim.x) sig_tab[i] = 0;
+    if constexpr (W == 1 && !MMW && ETWG_WARP_DEDUP)
+        for (int i = threadIdx.x; i < kDDSlots * (kThreads / 32); i += blockDim.x) {
+            dd_keys[i] = 0;
+            dd_rank[i] = ~0u;
+        }
     __syncthreads();
     // warp-granular: no block barrier inside the loop, so a warp whose
     // parents are cheap never waits for the CTA's slowest warp
@@ -457,9 +472,68 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         } else {
             M = warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         }
+        Set<W> Me = M;  // the children this lane emits
+#if ETWG_WARP_DEDUP
+        if constexpr (W == 1 && !MMW) {
+            // Warp pre-dedup: the warp's ~400 children go through a warp-
+            // private shared table (key -> min local rank lane*64+v, which
+            // orders like the global rank idx*64+v inside the warp); only a
+            // key's min-rank child in the warp is emitted. A child beaten
+            // inside the warp cannot be its key's global min-rank emission,
+            // so the global dedup and every counter are unchanged; keys that
+            // find no room are emitted as they are.
+            u64* tk = dd_keys + (threadIdx.x >> 5) * kDDSlots;
+            unsigned* tr = dd_rank + (threadIdx.x >> 5) * kDDSlots;
+            u64 rest = M.w[0];
+            while (rest) {
+                const int v = 63 - __clzll(rest);
+                rest ^= u64{1} << v;
+                const u64 key = S.w[0] | (u64{1} << v);
+                unsigned h = static_cast<unsigned>(fmix64(key)) & (kDDSlots - 1);
+                for (int probe = 0; probe < 8; ++probe) {
+                    const u64 seen = *reinterpret_cast<volatile u64*>(tk + h);
+                    bool mine = seen == key;
+                    if (seen == 0) {
+                        const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(tk + h), 0ull, key);
+                        mine = prev == 0 || prev == key;
+                    }
+                    if (mine) {
+                        atomicMin(tr + h, static_cast<unsigned>((lane << 6) | v));
+                        break;
+                    }
+                    h = (h + 1) & (kDDSlots - 1);
+                }
+            }
+            __syncwarp();
+            rest = M.w[0];
+            u64 keep = M.w[0];
+            while (rest) {
+                const int v = 63 - __clzll(rest);
+                rest ^= u64{1} << v;
+                const u64 key = S.w[0] | (u64{1} << v);
+                unsigned h = static_cast<unsigned>(fmix64(key)) & (kDDSlots - 1);
+                for (int probe = 0; probe < 8; ++probe) {
+                    const u64 seen = tk[h];
+                    if (seen == key) {
+                        if (tr[h] != static_cast<unsigned>((lane << 6) | v)) keep ^= u64{1} << v;
+                        break;
+                    }
+                    if (seen == 0) break;
+                    h = (h + 1) & (kDDSlots - 1);
+                }
+            }
+            __syncwarp();
+            for (int i = lane; i < kDDSlots; i += 32) {
+                tk[i] = 0;
+                tr[i] = ~0u;
+            }
+            __syncwarp();
+            Me.w[0] = keep;
+        }
+#endif
         if (pl.pass == 0) {  // counters and mask clear once per round, not per pass
             offered += M.count();
-            winners += M.count();
+            winners += Me.count();
             if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
         }
         bool full = false;
@@ -468,7 +542,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         // bucket-cursor atomics are in flight together; no flattening
         // shuffles (the trip count is the warp's largest child count)
         {
-            Set<W> rest = M;
+            Set<W> rest = Me;
             constexpr int LU = ETWG_LANE_UNROLL;
             while (rest.any()) {
                 Set<W> key[LU];
@@ -561,7 +635,10 @@ constexpr int kPartThreads = 512;
 
 // dynamic shared memory of k_exact_scatter<W, false, *> (candidates_sig tables)
 template <int W>
-constexpr int scatter_smem() { return W == 1 && ETWG_K1 == 3 ? sig_smem_bytes(kThreads) : 0; }
+constexpr int scatter_smem() {
+    return W == 1 && ETWG_K1 == 3 ? sig_smem_bytes(kThreads)
+                                  : (W == 1 && ETWG_WARP_DEDUP ? kDDSlots * (kThreads / 32) * 12 : 0);
+}
 
 // BLOOM: the round's distinct keys then meet the reference's Bloom filter
 // (bit positions (h1 + i*h2) mod m, bloom.cpp:86-97), each exactly once, so
