@@ -144,6 +144,9 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_EMIT_FLAT
 #define ETWG_EMIT_FLAT 0  // 1: children flattened over the warp's lanes; 0: each lane emits its own (-0.8 %)
 #endif
+#ifndef ETWG_PART_TMA
+#define ETWG_PART_TMA 0  // 1: k_exact_part_tma (cp.async.bulk staging) for one-word keys
+#endif
 #ifndef ETWG_WARP_DEDUP
 #define ETWG_WARP_DEDUP 0  // 1: warp-private pre-dedup of children before the bucket scatter
 #endif
@@ -644,6 +647,158 @@ constexpr int scatter_smem() {
 // (bit positions (h1 + i*h2) mod m, bloom.cpp:86-97), each exactly once, so
 // "any probed bit was clear" is the novelty test; keys the filter calls
 // duplicates (false positives) are dropped as the reference drops them.
+// ----------------------------------------------------------------------
+// k_exact_part_tma (one-word keys, 16-byte records): the same per-bucket
+// min-rank dedup as k_exact_part, with each bucket's contiguous records
+// staged into shared memory by the Blackwell bulk-copy engine
+// (cp.async.bulk, 1D TMA, completion on an mbarrier): two 24 KB stages in
+// flight, the next bucket's first two chunks issued before the current
+// bucket's mark pass, so no thread waits on a global load. Two 112 KB CTAs
+// per SM.
+constexpr int kTmaChunk = 1536;  // records per stage (24 KB)
+constexpr int kTmaThreads = 512;
+constexpr int tma_part_smem_bytes() { return part_smem_bytes<1>() + 2 * kTmaChunk * 16 + 16; }
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, u64* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bar_wait(u64* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <bool BLOOM>
+__global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params* __restrict__ P, Control* C, Bufs B) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int SLOTS = part_slots<1>();
+    u64* keys = reinterpret_cast<u64*>(smem_raw);
+    u64* ranks = keys + SLOTS;
+    u64* stage = ranks + SLOTS;                      // [2][kTmaChunk * 2] u64
+    u64* bars = stage + 2 * kTmaChunk * 2;           // 2 mbarriers
+    __shared__ unsigned s_full;
+    if (halted(C)) return;
+    const unsigned r = C->round;
+    if (C->rs[r].compact) return;
+    const u64 passes = C->passes ? C->passes : 1;
+    const u64 pass = C->pass;
+    const u64 np = C->rs[r].np / passes;
+    const u64 cap = C->rs[r].pcap;
+    u64 probed = 0;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bars)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bars + 1)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned phase[2] = {0, 0};
+    auto count_of = [&](u64 lp) -> unsigned {
+        const unsigned c = B.cursors[lp * passes + pass];
+        return c < cap ? c : static_cast<unsigned>(cap);
+    };
+    // issues chunks [c0, c0+2) of local bucket lp into the stages (thread 0)
+    auto issue = [&](u64 lp, unsigned cnt, unsigned c0) {
+        const u64* recs = B.recs + lp * cap * 2;
+        for (unsigned c = c0; c < c0 + 2; ++c) {
+            const unsigned first = c * kTmaChunk;
+            if (first >= cnt) break;
+            const unsigned n = min(cnt - first, static_cast<unsigned>(kTmaChunk));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(stage + (c & 1) * kTmaChunk * 2, recs + 2 * static_cast<u64>(first), n * 16, bars + (c & 1));
+        }
+    };
+    u64 lp = blockIdx.x;
+    if (lp < np && threadIdx.x == 0) issue(lp, count_of(lp), 0);
+    for (; lp < np; lp += gridDim.x) {
+        const u64 part = lp * passes + pass;
+        const unsigned cnt = count_of(lp);
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+            keys[i] = 0;
+            ranks[i] = ~u64{0};
+        }
+        if (threadIdx.x == 0) s_full = 0;
+        __syncthreads();
+        const unsigned nch = (cnt + kTmaChunk - 1) / kTmaChunk;
+        for (unsigned c = 0; c < nch; ++c) {
+            const int st = c & 1;
+            bar_wait(bars + st, phase[st]);
+            phase[st] ^= 1;
+            const unsigned n = min(cnt - c * kTmaChunk, static_cast<unsigned>(kTmaChunk));
+            const u64* sb = stage + st * kTmaChunk * 2;
+            for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+                const ulonglong2 rec = *reinterpret_cast<const ulonglong2*>(sb + 2 * i);
+                Set<1> key;
+                key.w[0] = rec.x;
+                const u64 rank = rec.y;
+                unsigned h = static_cast<unsigned>(slot_hash<1>(key)) & (SLOTS - 1);
+                bool placed = false;
+                for (int probe = 0; probe < 128 && !placed; ++probe) {
+                    placed = smem_claim<1>(keys, h, key);
+                    if (!placed) h = (h + 1) & (SLOTS - 1);
+                }
+                if (placed && rank < *reinterpret_cast<volatile u64*>(ranks + h))
+                    atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), rank);
+                if (!placed) s_full = 1;
+            }
+            __syncthreads();  // stage st consumed by every thread
+            if (threadIdx.x == 0 && c + 2 < nch) issue(lp, cnt, c + 2);
+        }
+        if (s_full) {  // block-uniform; no load is in flight here
+            if (threadIdx.x == 0) {
+                C->need = 2 * np * passes;
+                C->abort = kGrowParts;
+            }
+            break;
+        }
+        // both stages free: start the next bucket's loads under this bucket's mark pass
+        const u64 nxt = lp + gridDim.x;
+        if (threadIdx.x == 0 && nxt < np) issue(nxt, count_of(nxt), 0);
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+            const u64 rank = ranks[i];
+            if (rank == ~u64{0}) continue;
+            if constexpr (BLOOM) {
+                Set<1> key;
+                key.w[0] = keys[i];
+                const u64 m = bloom_bits_for(round_cap(*P, C->count[r & 1]), P->bpe);
+                unsigned* bits = B.bloom[r & 1];
+                const unsigned h1 = murmur_key<1>(key, kSeed1);
+                const unsigned h2 = murmur_key<1>(key, kSeed2);
+                u64 pos, step;
+                probe_start(h1, h2, m, pos, step);
+                ++probed;
+                if (!bloom_or_probes(bits, m, pos, step, P->hashes)) {
+                    atomicAdd(&C->rs[r].fp, 1ull);
+                    continue;
+                }
+            }
+            const u64 parent = rank / 64;
+            const int v = static_cast<int>(rank % 64);
+            atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + parent, u64{1} << v);
+        }
+        if (threadIdx.x == 0) B.cursors[part] = 0;
+        __syncthreads();
+    }
+    if (BLOOM) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) probed += __shfl_xor_sync(kFull, probed, o);
+        if ((threadIdx.x & 31) == 0 && probed) atomicAdd(&C->rs[r].probed, probed);
+    }
+}
+
 template <int W, bool BLOOM>
 __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __restrict__ P, Control* C, Bufs B) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1386,6 +1541,7 @@ private:
     }();
     int grid_part_[2] = {0, 0};
     int grid_compact_ = 0;
+    int grid_tma_ = 0;
     bool compact_possible_ = false;  // ETWG_COMPACT build or ETWG_DEBUG 8192 this decide
     unsigned passes_ = 1;            // hash-range passes per round (f4: records beyond HBM)
     bool part_bloom_ = false;  // Bloom rounds of this decide use scatter/part/append
@@ -1521,6 +1677,17 @@ private:
             allow_part(k_exact_part<1, true>, part_smem_bytes<1>(), g);
             allow_part(k_exact_part<2, true>, part_smem_bytes<2>(), g);
             allow_part(k_exact_part_compact<false>, compact_smem_bytes(), grid_compact_);
+            auto allow_tma = [&](auto kernel, int& grid) {
+                check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_part_smem_bytes()),
+                      "smem attribute");
+                int blocks = 0;
+                check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kTmaThreads, tma_part_smem_bytes()),
+                      "occupancy");
+                grid = prop.multiProcessorCount * std::max(1, blocks);
+            };
+            allow_tma(k_exact_part_tma<false>, grid_tma_);
+            allow_tma(k_exact_part_tma<true>, g);
+            grid_tma_ = std::min(grid_tma_, g);
             allow_part(k_exact_part_compact<true>, compact_smem_bytes(), g);
             grid_compact_ = std::min(grid_compact_, g);
         }
@@ -1745,8 +1912,12 @@ private:
             else
                 timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.expand_ms, prof.t.expand_launches);
-            timed_launch([&] { k_exact_part<W, BLOOM><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
-                         prof.t.insert_ms, prof.t.insert_launches);
+            if (W == 1 && ETWG_PART_TMA)
+                timed_launch([&] { k_exact_part_tma<BLOOM><<<grid_tma_, kTmaThreads, tma_part_smem_bytes(), stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.insert_ms, prof.t.insert_launches);
+            else
+                timed_launch([&] { k_exact_part<W, BLOOM><<<grid_part_[W - 1], kPartThreads, part_smem_bytes<W>(), stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.insert_ms, prof.t.insert_launches);
             if (W == 1 && compact_possible_)  // the plan picks one record format; the other kernel returns at once
                 timed_launch([&] { k_exact_part_compact<BLOOM><<<grid_compact_, kPartThreads, compact_smem_bytes(), stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.insert_ms, prof.t.insert_launches);
