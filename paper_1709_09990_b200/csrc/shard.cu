@@ -125,6 +125,7 @@ struct Plan {
     int lg, G, me, rounds;
     int shared_r;   // k_route keeps K1's boundary tables in (dynamic) shared memory
     int emit;       // emitter-stored layers: records carry (index << 7 | vertex), no history
+    int direct;     // emitter-stored: owners OR each winner straight into the emitter's mask
 };
 
 struct ShardBufs {
@@ -159,6 +160,9 @@ struct ShardBufs {
     const u64* src_marks[kMaxShards];       // owner o's marks for this shard
     const unsigned* src_mark_cnt[kMaxShards];
     u64* cmask;          // u64[W] per local parent
+    // direct marks: every emitter's winner masks (virtual shards: the other
+    // shard's buffer; NVLink: the peer's mask mapped over CUDA IPC)
+    u64* dst_cmask[kMaxShards];
 };
 
 template <int W>
@@ -545,6 +549,32 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner_emit(const Params* __re
             if (threadIdx.x == 0) {
                 atomicOr(&C->mine.abort, static_cast<unsigned>(kAbortParts));
                 atomicMax(&C->mine.need_parts, 2 * pl.np);
+            }
+            __syncthreads();
+            continue;
+        }
+        if (pl.direct) {
+            // winners (Bloom: those the owner's filter calls novel) set their
+            // bit in the emitting shard's winner mask directly — a local or
+            // NVLink peer atomic — instead of a mark list the emitter applies
+            for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+                const u64 rank = ranks[i];
+                if (rank == ~u64{0}) continue;
+                if constexpr (BLOOM) {
+                    Set<W> key;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) key.w[w] = keys[W * i + w];
+                    const unsigned h1 = murmur_key<W>(key, kSeed1);
+                    const unsigned h2 = murmur_key<W>(key, kSeed2);
+                    u64 pos, step;
+                    probe_start(h1, h2, pl.bloom_m, pos, step);
+                    if (!bloom_or_probes(B.bloom, pl.bloom_m, pos, step, P->hashes)) continue;
+                }
+                const int emitter = static_cast<int>(((rank >> 40) + pl.me) % pl.G);
+                const u64 m = rank & ((u64{1} << 40) - 1);
+                const int v = static_cast<int>(m & 127);
+                atomicOr(reinterpret_cast<unsigned long long*>(B.dst_cmask[emitter]) + (m >> 7) * W + (v >> 6),
+                         u64{1} << (v & 63));
             }
             __syncthreads();
             continue;
@@ -1208,6 +1238,11 @@ private:
     const u64* peer_out_[kMaxShards] = {};
     const unsigned* peer_cnt_[kMaxShards] = {};
     const u64* peer_marks_[kMaxShards] = {};
+    u64* peer_cmask_[kMaxShards] = {};
+    bool direct_request_ = [] {  // ETWG_DIRECT_MARKS=0: owners return mark lists instead
+        const char* e = std::getenv("ETWG_DIRECT_MARKS");
+        return !(e && e[0] == '0');
+    }();
     const unsigned* peer_mark_cnt_[kMaxShards] = {};
     unsigned char* d_handles_ = nullptr;
 
@@ -1461,6 +1496,7 @@ private:
         pl.cap = std::max<u64>(per + per / 4 + 64, cap_floor_);
         pl.layer_est = per_owner + per_owner / 4 + 1024;
         pl.emit = emit_ ? 1 : 0;
+        pl.direct = 0;  // decided per launch (launch_owner_emit): needs every emitter's mask mapped
         mark_cap_plan_ = std::max<u64>(per_owner + per_owner / 2 + 4096, mark_floor_);
         if (tight_) {  // tests: undersized plans, so rounds abort, grow and re-run
             pl.np = std::max<u64>(std::max<u64>(pl.np / 16, 1), np_floor_);
@@ -1567,6 +1603,7 @@ private:
                 cudaFree(s.b.cmask);
                 check(cudaMalloc(&s.b.cmask, s.b.layer_cap * 16), "winner masks");
                 s.cmask_cap = s.b.layer_cap;
+                handles_dirty_ = true;  // peers map the masks for direct marks
             }
             const u64 tiles_needed = (count[s.me] + emit_span(W) - 1) / emit_span(W) + 2;
             if (tiles_needed > s.b.tile_cap) {
@@ -1681,9 +1718,21 @@ private:
         }
     }
 
+    // direct marks: every emitter's winner mask reachable from this shard
+    bool direct_marks(Shard& s) {
+        if (!direct_request_) return false;
+        for (int e = 0; e < G_; ++e) {
+            u64* m = !comm_ ? local_[e].b.cmask : (e == s.me ? s.b.cmask : (p2p_ ? peer_cmask_[e] : nullptr));
+            if (!m) return false;
+            s.b.dst_cmask[e] = m;
+        }
+        return true;
+    }
+
     void launch_owner_emit(Shard& s, const Plan& pl, int W, bool bloom) {
         Plan p = pl;
         p.me = s.me;
+        p.direct = direct_marks(s) ? 1 : 0;
         set_sources(s, pl, W);
         if (W == 1) {
             if (bloom) k_owner_emit<1, true><<<grid_owner_[0], kOwnerThreads, owner_smem_bytes<1>(), stream_>>>(s.d_params, s.d_ctl, s.b, p);
@@ -1713,11 +1762,12 @@ private:
             }
         }
         const int grid = grid_route_[0];
+        const bool direct = direct_marks(s);  // the owners already set the winner bits
         if (W == 1) {
-            k_apply_marks<1><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
+            if (!direct) k_apply_marks<1><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
             k_emit_append<1><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
         } else {
-            k_apply_marks<2><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
+            if (!direct) k_apply_marks<2><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
             k_emit_append<2><<<grid, kRouteThreads, 0, stream_>>>(s.d_ctl, s.b, p);
         }
         check(cudaGetLastError(), "emit append launch");
@@ -1791,8 +1841,8 @@ private:
     // bucket counts and maps its peers'. If any rank fails to map, all fall
     // back to the NCCL send/recv exchange.
     struct IpcRecord {
-        cudaIpcMemHandle_t out, cnt, marks, mark_cnt;
-        int ok, has_marks, pad[2];
+        cudaIpcMemHandle_t out, cnt, marks, mark_cnt, cmask;
+        int ok, has_marks, has_cmask, pad;
     };
 
     void share_outboxes(Shard& s) {
@@ -1812,6 +1862,8 @@ private:
         if (mine.has_marks)
             mine.ok = mine.ok && ok_or(cudaIpcGetMemHandle(&mine.marks, s.b.marks)) &&
                       ok_or(cudaIpcGetMemHandle(&mine.mark_cnt, s.b.mark_cnt));
+        mine.has_cmask = emit_ && s.b.cmask;
+        if (mine.has_cmask) mine.ok = mine.ok && ok_or(cudaIpcGetMemHandle(&mine.cmask, s.b.cmask));
         cudaGetLastError();
         check(cudaMemcpyAsync(d_handles_ + rec * s.me, &mine, rec, cudaMemcpyHostToDevice, stream_), "ipc h2d");
         nc.check(nc.AllGather(d_handles_ + rec * s.me, d_handles_, rec, ncclUint8, comm_, stream_), "ipc allgather");
@@ -1850,6 +1902,15 @@ private:
                 peer_marks_[p] = static_cast<const u64*>(c);
                 peer_mark_cnt_[p] = static_cast<const unsigned*>(d);
             }
+            if (h[p].has_cmask) {
+                void* e = nullptr;
+                if (!ok_or(cudaIpcOpenMemHandle(&e, h[p].cmask, cudaIpcMemLazyEnablePeerAccess))) {
+                    cudaGetLastError();
+                    ok = 0;
+                    break;
+                }
+                peer_cmask_[p] = static_cast<u64*>(e);
+            }
         }
         if (trace_) std::fprintf(stderr, "[shard %d] opened: ok=%d (%s)\n", s.me, ok, cudaGetErrorString(why));
         // agree: p2p only if every rank mapped every peer
@@ -1878,6 +1939,8 @@ private:
             if (peer_out_[p]) cudaIpcCloseMemHandle(const_cast<u64*>(peer_out_[p]));
             if (peer_cnt_[p]) cudaIpcCloseMemHandle(const_cast<unsigned*>(peer_cnt_[p]));
             if (peer_marks_[p]) cudaIpcCloseMemHandle(const_cast<u64*>(peer_marks_[p]));
+            if (peer_cmask_[p]) cudaIpcCloseMemHandle(peer_cmask_[p]);
+            peer_cmask_[p] = nullptr;
             if (peer_mark_cnt_[p]) cudaIpcCloseMemHandle(const_cast<unsigned*>(peer_mark_cnt_[p]));
             peer_out_[p] = nullptr;
             peer_cnt_[p] = nullptr;

@@ -263,7 +263,7 @@ print(json.dumps(res))
 """
 
 
-def _tight_run(tight, handoff, mode="emitter"):
+def _tight_run(tight, handoff, mode="emitter", extra=None):
     import os
     import subprocess
     import sys
@@ -271,6 +271,7 @@ def _tight_run(tight, handoff, mode="emitter"):
     env.pop("ETWG_SHARD_TIGHT", None)
     if tight:
         env["ETWG_SHARD_TIGHT"] = "1"
+    env.update(extra or {})
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", _TIGHT_CODE, str(handoff), mode], env=env, cwd=root,
                          capture_output=True, text=True, timeout=900)
@@ -292,3 +293,19 @@ def test_sharded_rounds_survive_aborts(gpu, handoff, mode):
         assert tight[key][1] == normal[key][1], key
         if key != "b":  # Bloom layers depend on the order keys meet the filter
             assert tight[key][2] == normal[key][2], key
+
+
+@pytest.mark.parametrize("handoff", [0, 3000])
+def test_direct_marks_equal_mark_lists(gpu, handoff):
+    """Emitter-stored layers: by default each owner ORs its winners straight
+    into the emitting shard's winner mask (same device or an NVLink peer
+    mapping); ETWG_DIRECT_MARKS=0 returns mark lists the emitter applies.
+    Counters and layer sets are identical, also under forced aborts."""
+    lists = _tight_run(False, handoff, extra={"ETWG_DIRECT_MARKS": "0"})
+    direct = _tight_run(False, handoff)
+    lists.pop("reruns")
+    direct.pop("reruns")
+    assert direct == lists
+    tight = _tight_run(True, handoff)
+    tight.pop("reruns")
+    assert tight == lists
