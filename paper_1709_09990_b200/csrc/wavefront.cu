@@ -710,10 +710,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
         const unsigned c = B.cursors[lp * passes + pass];
         return c < cap ? c : static_cast<unsigned>(cap);
     };
-    // issues chunks [c0, c0+2) of local bucket lp into the stages (thread 0)
-    auto issue = [&](u64 lp, unsigned cnt, unsigned c0) {
+    // issues chunks [c0, c0+k) of local bucket lp into their stages (thread 0)
+    auto issue = [&](u64 lp, unsigned cnt, unsigned c0, unsigned k) {
         const u64* recs = B.recs + lp * cap * 2;
-        for (unsigned c = c0; c < c0 + 2; ++c) {
+        for (unsigned c = c0; c < c0 + k; ++c) {
             const unsigned first = c * kTmaChunk;
             if (first >= cnt) break;
             const unsigned n = min(cnt - first, static_cast<unsigned>(kTmaChunk));
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
         }
     };
     u64 lp = blockIdx.x;
-    if (lp < np && threadIdx.x == 0) issue(lp, count_of(lp), 0);
+    if (lp < np && threadIdx.x == 0) issue(lp, count_of(lp), 0, 2);
     for (; lp < np; lp += gridDim.x) {
         const u64 part = lp * passes + pass;
         const unsigned cnt = count_of(lp);
@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
                 if (!placed) s_full = 1;
             }
             __syncthreads();  // stage st consumed by every thread
-            if (threadIdx.x == 0 && c + 2 < nch) issue(lp, cnt, c + 2);
+            if (threadIdx.x == 0 && c + 2 < nch) issue(lp, cnt, c + 2, 1);
         }
         if (s_full) {  // block-uniform; no load is in flight here
             if (threadIdx.x == 0) {
@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
         }
         // both stages free: start the next bucket's loads under this bucket's mark pass
         const u64 nxt = lp + gridDim.x;
-        if (threadIdx.x == 0 && nxt < np) issue(nxt, count_of(nxt), 0);
+        if (threadIdx.x == 0 && nxt < np) issue(nxt, count_of(nxt), 0, 2);
         for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
             const u64 rank = ranks[i];
             if (rank == ~u64{0}) continue;
