@@ -145,7 +145,7 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #define ETWG_EMIT_FLAT 0  // 1: children flattened over the warp's lanes; 0: each lane emits its own (-0.8 %)
 #endif
 #ifndef ETWG_PART_TMA
-#define ETWG_PART_TMA 0  // 1: k_exact_part_tma (cp.async.bulk staging) for one-word keys
+#define ETWG_PART_TMA 1  // 1: k_exact_part_tma (cp.async.bulk staging) for exact rounds of one-word keys
 #endif
 #ifndef ETWG_WARP_DEDUP
 #define ETWG_WARP_DEDUP 0  // 1: warp-private pre-dedup of children before the bucket scatter
@@ -1912,7 +1912,7 @@ private:
             else
                 timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.expand_ms, prof.t.expand_launches);
-            if (W == 1 && ETWG_PART_TMA)
+            if (W == 1 && ETWG_PART_TMA && !BLOOM)  // Bloom probes want the 3-CTA kernel's warps
                 timed_launch([&] { k_exact_part_tma<BLOOM><<<grid_tma_, kTmaThreads, tma_part_smem_bytes(), stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.insert_ms, prof.t.insert_launches);
             else
