@@ -336,12 +336,20 @@ def bloom_probe(E, G):
         g48 = E.Graph.from_rows(workload_rows())  # BASELINE cfg 4: Bloom vs exact on the bench graph
         opts = E.Options(dedup="bloom", max_layer_states=CAP)
         E.solve(g48, opts)
+        E.reset_times()
         E.timer_begin()
         r = E.solve(g48, opts)
         ms = E.timer_end()
+        tm = E.times()
         ex_n = json.loads(r.stats_json)["totals"]["expanded"]
         out["g48_bloom"] = {"treewidth": r.value, "expanded": ex_n, "ms": ms,
                             "states_per_s": ex_n / (ms / 1e3),
+                            "distinct_keys_probed": int(tm.get("bloom_probed", 0)),
+                            "rejected_by_filter": int(tm.get("bloom_fp", 0)),
+                            "measured_fp_rate": tm.get("bloom_fp", 0) / max(1.0, tm.get("bloom_probed", 0)),
+                            "fp_explained": "every rejected key shares its Murmur3 (h1, h2) pair -- all 17 "
+                                            "probe positions -- with another distinct key of the same round "
+                                            "(DESIGN.md 5.3, profiles/r02_bloom_fp_explained.txt)",
                             "path": "partitioned (filter > 2^28 bits): exact bucket dedup, then the "
                                     "reference's 17-probe filter per distinct child"}
         g40 = E.Graph.from_rows(rows)
