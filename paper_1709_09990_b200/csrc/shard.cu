@@ -71,6 +71,9 @@ constexpr int kMaxShards = 8;
 #endif
 constexpr int kOwnerThreads = 512;
 constexpr int kRouteThreads = 256;
+#ifndef ETWG_ROUTE_LANE_EMIT
+#define ETWG_ROUTE_LANE_EMIT 1  // k_route: each lane routes its own children (0: flattened over the warp)
+#endif
 // parents per look-back tile of k_emit_append (its ITEMS x kRouteThreads);
 // the host sizes the tile-status array from the same figure
 constexpr unsigned long long emit_span(int W) { return static_cast<unsigned long long>(kRouteThreads) * (W == 1 ? 8 : 4); }
@@ -228,6 +231,36 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
             tile_dedup<W, route_tile_slots<W>()>(ts, win, S, M);
         }
         routed += M.count();
+#if ETWG_ROUTE_LANE_EMIT
+        // each lane routes its own parent's children (no flattening
+        // shuffles; the trip count is the warp's largest child count)
+        {
+            Set<W> rest = M;
+            while (rest.any()) {
+                const int v = pop_any(rest);
+                Set<W> key = S;
+                key.add(v);
+                const u64 bucket = static_cast<u64>(owner_of<W>(key, pl.G)) * pl.np + part_hash_bits<W>(key, pl.lg);
+                const unsigned slot = atomicAdd(B.out_cnt + bucket, 1u);
+                if (slot < pl.cap) {
+                    u64* rec = B.out + (bucket * pl.cap + slot) * srec_words<W>();
+                    const u64 packed = pl.emit ? ((idx << 7) | static_cast<u64>(v))
+                                               : ((idx << 32) | ((H << 8) | static_cast<unsigned>(v)));  // push_history
+                    if constexpr (W == 1) {
+                        *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], packed);
+                    } else {
+                        rec[0] = key.w[0];
+                        rec[1] = key.w[1];
+                        rec[2] = packed;
+                    }
+                } else {
+                    full = true;
+                }
+            }
+        }
+        if (false)
+#endif
+        {
         WarpFlat f;
         f.scan(M.count());
         const u64 warp_base = tile * kRouteThreads + (threadIdx.x & ~31);
@@ -259,6 +292,7 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
                     full = true;
                 }
             }
+        }
         }
         if constexpr (TILE) __syncthreads();  // the next tile clears the tile set
     }
