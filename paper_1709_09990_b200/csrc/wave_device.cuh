@@ -382,7 +382,7 @@ __device__ __forceinline__ Set<W> candidates_shared(const Set<W>* adj, int k, co
 // number, the same for every lane), and the candidate loop runs over the
 // eligible set, whose size n - |S| - |forbidden| is also warp-uniform.
 #ifndef ETWG_K1
-#define ETWG_K1 4  // 4: half-word register slots (one-word keys); 2: register slots + isolated-member loop; 3: shared signatures; 1: per-vertex table
+#define ETWG_K1 4  // 4: half-word register slots (one-word keys); 2: register slots + isolated-member loop; 1: per-vertex table
 #endif
 #ifndef ETWG_K1_LOOP
 #define ETWG_K1_LOOP 2  // 1: two 32-bit half loops with an early |N(v) \ S| > k exit
@@ -497,23 +497,6 @@ __device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, con
     return keep;
 }
 
-// K1 with per-vertex component signatures (one-word keys, thread per
-// parent). Each component of G[S] whose boundary B_j meets the eligible set
-// (isolated members included, B = N(u)) gets an index j < kSigComps; its
-// boundary goes to the thread's row Bs[j] and every v in B_j gets bit j in
-// the thread's signature sig[v] (both in shared memory, strided by the block
-// size so a warp's accesses are lane-consecutive). A candidate then ORs
-// exactly the boundaries it touches, Q(S,v) = N(v)\S + the B_j of the set
-// bits of sig[v] (graph.hpp:61-78), one shared load per touched component
-// instead of a test of every component. Boundaries above k+1 vertices reject
-// their vertices as a mask. More than kSigComps components (rare) falls back
-// to the register-slot K1 for that parent.
-#ifndef ETWG_SIG_COMPS
-#define ETWG_SIG_COMPS 12
-#endif
-constexpr int kSigComps = ETWG_SIG_COMPS;
-constexpr int sig_smem_bytes(int threads) { return threads * (kSigComps * 8 + 64 * 2); }
-
 // K1 for one-word keys with every relevant component in a register slot
 // (isolated members too: their boundary is their row), held as 32-bit halves.
 // The candidate loop runs once over the low and once over the high half of
@@ -596,99 +579,6 @@ __device__ __forceinline__ u64 candidates_half(const Set<1>* adj, int k, u64 S, 
             }
             if (h) qhi &= ~bit; else qlo &= ~bit;
             if (__popc(qlo) + __popc(qhi) <= k) keep |= u64{1} << v;
-        }
-    }
-    return keep;
-}
-
-// the rare overflow path of candidates_sig, out of line so its registers
-// do not count against the common path
-__device__ __noinline__ u64 candidates_slots_w1(const Set<1>* adj, int k, u64 S, u64 eligible) {
-    Set<1> s1, e1;
-    s1.w[0] = S;
-    e1.w[0] = eligible;
-    return candidates_slots<1>(adj, k, s1, e1).w[0];
-}
-
-__device__ __forceinline__ Set<1> candidates_sig(const Set<1>* adj, int k, const Set<1>& S, const Set<1>& eligible,
-                                                 u64* Bs, unsigned short* sig) {
-    const int T = blockDim.x;
-    const int t = threadIdx.x;
-    const u64 s0 = S.w[0];
-    u64 reject = 0, touched = 0;
-    int nc = 0;
-    bool overflow = false;
-    u64 rem = s0, frontier = 0, nb = 0, comp = 0;
-    const int r = __popcll(s0);
-    for (int it = 0; it < r; ++it) {
-        if (!frontier) {
-            const int seed = 63 - __clzll(rem);
-            frontier = u64{1} << seed;
-            rem ^= frontier;
-            comp = frontier;
-            nb = 0;
-        }
-        const int x = 63 - __clzll(frontier);
-        frontier ^= u64{1} << x;
-        const u64 a = adj[x].w[0];
-        nb |= a;
-        const u64 fresh = a & rem;
-        rem ^= fresh;
-        comp |= fresh;
-        frontier |= fresh;
-        if (frontier) continue;
-        const u64 B = nb & ~s0;
-        if (!(B & eligible.w[0])) continue;
-        if (__popcll(B) > k + 1) {
-            reject |= B;
-            continue;
-        }
-        if (nc == kSigComps) {
-            overflow = true;
-            continue;
-        }
-        Bs[nc * T + t] = B;
-        touched |= B;
-        const unsigned short bit = static_cast<unsigned short>(1u << nc);
-        for (int h = 0; h < 2; ++h) {
-            unsigned y = static_cast<unsigned>(B >> (32 * h));
-            while (y) {
-                const int b = 31 - __clz(y);
-                y ^= 1u << b;
-                sig[(32 * h + b) * T + t] |= bit;
-            }
-        }
-        ++nc;
-    }
-    Set<1> keep = Set<1>::zero();
-    if (overflow) {
-        keep.w[0] = candidates_slots_w1(adj, k, S.w[0], eligible.w[0]);
-    } else {
-        const u64 cand = eligible.w[0] & ~reject;
-        for (int h = 0; h < 2; ++h) {
-            unsigned y = static_cast<unsigned>(cand >> (32 * h));
-            while (y) {
-                const int b = 31 - __clz(y);
-                y ^= 1u << b;
-                const int v = 32 * h + b;
-                unsigned sg = sig[v * T + t];
-                u64 q = adj[v].w[0] & ~s0;
-                while (sg) {
-                    const int j = __ffs(sg) - 1;
-                    sg &= sg - 1;
-                    q |= Bs[j * T + t];
-                }
-                q &= ~(u64{1} << v);
-                if (__popcll(q) <= k) keep.w[0] |= u64{1} << v;
-            }
-        }
-    }
-    for (int h = 0; h < 2; ++h) {  // leave the signature table clear for the next parent
-        unsigned y = static_cast<unsigned>(touched >> (32 * h));
-        while (y) {
-            const int b = 31 - __clz(y);
-            y ^= 1u << b;
-            sig[(32 * h + b) * T + t] = 0;
         }
     }
     return keep;

@@ -147,18 +147,8 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_PART_TMA
 #define ETWG_PART_TMA 1  // 1: k_exact_part_tma (cp.async.bulk staging) for exact rounds of one-word keys
 #endif
-#ifndef ETWG_WARP_DEDUP
-#define ETWG_WARP_DEDUP 0  // 1: warp-private pre-dedup of children before the bucket scatter
-#endif
-#ifndef ETWG_DD_SLOTS
-#define ETWG_DD_SLOTS 512
-#endif
-constexpr int kDDSlots = ETWG_DD_SLOTS;
 #ifndef ETWG_LANE_UNROLL
 #define ETWG_LANE_UNROLL 2  // children per lane whose bucket-cursor atomics are in flight together
-#endif
-#ifndef ETWG_REC_EVICT_LAST
-#define ETWG_REC_EVICT_LAST 0  // 1: child records stored with an L2 evict-last hint
 #endif
 #ifndef ETWG_COMPACT
 #define ETWG_COMPACT 0  // 1: 8-byte records on every eligible round (see PartPlan)
@@ -325,18 +315,7 @@ __device__ __forceinline__ void record_store(const Bufs& B, const PartPlan& pl, 
     }
     u64* rec = B.recs + (lp * pl.cap + slot) * rec_words<W>();
     if constexpr (W == 1) {
-#if ETWG_REC_EVICT_LAST
-        // keep the bucket tails in L2 until both halves of each 32-byte
-        // sector are written (a partial sector evicted costs a DRAM
-        // read-modify-write)
-        u64 pol;
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-        asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(rec), "l"(key.w[0]),
-                     "l"(child_rank<W>(parent, v)), "l"(pol)
-                     : "memory");
-#else
         *reinterpret_cast<ulonglong2*>(rec) = make_ulonglong2(key.w[0], child_rank<W>(parent, v));
-#endif
     } else {
         *reinterpret_cast<ulonglong4*>(rec) = make_ulonglong4(key.w[0], key.w[1], child_rank<W>(parent, v), 0);
     }
@@ -357,14 +336,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                                                             Bufs B) {
     __shared__ Set<W> adj[64 * W];
     __shared__ unsigned mmw_keep[MMW ? kThreads : 1][2 * W];
-    // ETWG_K1 3: per-thread component boundaries and vertex signatures
-    // (candidates_sig), dynamic shared memory, zeroed once per launch
-    extern __shared__ __align__(16) unsigned char scatter_dyn[];
-    u64* sig_bs = reinterpret_cast<u64*>(scatter_dyn);
-    unsigned short* sig_tab = reinterpret_cast<unsigned short*>(sig_bs + kSigComps * kThreads);
-    // ETWG_WARP_DEDUP: per-warp {key, min local rank} tables (same dynamic block)
-    u64* dd_keys = reinterpret_cast<u64*>(scatter_dyn);
-    unsigned* dd_rank = reinterpret_cast<unsigned*>(dd_keys + kDDSlots * (kThreads / 32));
+
     __shared__ Set<W> warp_tables[kThreads / 32][MMW ? 2 : 1][64 * W];  // small-layer mode
     if (halted(C)) return;
     const unsigned r = C->round;
@@ -411,13 +383,6 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     const Set<W> forbidden = param_set<W>(P->forbidden);
     const u64* in = B.keys[r & 1];
     load_adjacency<W>(P, adj);
-    if constexpr (W == 1 && !MMW && ETWG_K1 == 3)
-        for (int i = threadIdx.x; i < 64 * kThreads; i += blockDim.x) sig_tab[i] = 0;
-    if constexpr (W == 1 && !MMW && ETWG_WARP_DEDUP)
-        for (int i = threadIdx.x; i < kDDSlots * (kThreads / 32); i += blockDim.x) {
-            dd_keys[i] = 0;
-            dd_rank[i] = ~0u;
-        }
     __syncthreads();
     // warp-granular: no block barrier inside the loop, so a warp whose
     // parents are cheap never waits for the CTA's slowest warp
@@ -465,75 +430,9 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         const u64 idx = base + lane;
         const bool valid = idx < E;
         const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
-        Set<W> M;
-        if constexpr (W == 1 && !MMW && ETWG_K1 == 3) {
-            M = Set<W>::zero();
-            if (valid) {
-                const Set<1> open = Set<1>::prefix(P->n) - S;
-                M = candidates_sig(adj, P->k, S, open - forbidden, sig_bs, sig_tab);
-            }
-        } else {
-            M = warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
-        }
+        const Set<W> M =
+            warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         Set<W> Me = M;  // the children this lane emits
-#if ETWG_WARP_DEDUP
-        if constexpr (W == 1 && !MMW) {
-            // Warp pre-dedup: the warp's ~400 children go through a warp-
-            // private shared table (key -> min local rank lane*64+v, which
-            // orders like the global rank idx*64+v inside the warp); only a
-            // key's min-rank child in the warp is emitted. A child beaten
-            // inside the warp cannot be its key's global min-rank emission,
-            // so the global dedup and every counter are unchanged; keys that
-            // find no room are emitted as they are.
-            u64* tk = dd_keys + (threadIdx.x >> 5) * kDDSlots;
-            unsigned* tr = dd_rank + (threadIdx.x >> 5) * kDDSlots;
-            u64 rest = M.w[0];
-            while (rest) {
-                const int v = 63 - __clzll(rest);
-                rest ^= u64{1} << v;
-                const u64 key = S.w[0] | (u64{1} << v);
-                unsigned h = static_cast<unsigned>(fmix64(key)) & (kDDSlots - 1);
-                for (int probe = 0; probe < 8; ++probe) {
-                    const u64 seen = *reinterpret_cast<volatile u64*>(tk + h);
-                    bool mine = seen == key;
-                    if (seen == 0) {
-                        const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(tk + h), 0ull, key);
-                        mine = prev == 0 || prev == key;
-                    }
-                    if (mine) {
-                        atomicMin(tr + h, static_cast<unsigned>((lane << 6) | v));
-                        break;
-                    }
-                    h = (h + 1) & (kDDSlots - 1);
-                }
-            }
-            __syncwarp();
-            rest = M.w[0];
-            u64 keep = M.w[0];
-            while (rest) {
-                const int v = 63 - __clzll(rest);
-                rest ^= u64{1} << v;
-                const u64 key = S.w[0] | (u64{1} << v);
-                unsigned h = static_cast<unsigned>(fmix64(key)) & (kDDSlots - 1);
-                for (int probe = 0; probe < 8; ++probe) {
-                    const u64 seen = tk[h];
-                    if (seen == key) {
-                        if (tr[h] != static_cast<unsigned>((lane << 6) | v)) keep ^= u64{1} << v;
-                        break;
-                    }
-                    if (seen == 0) break;
-                    h = (h + 1) & (kDDSlots - 1);
-                }
-            }
-            __syncwarp();
-            for (int i = lane; i < kDDSlots; i += 32) {
-                tk[i] = 0;
-                tr[i] = ~0u;
-            }
-            __syncwarp();
-            Me.w[0] = keep;
-        }
-#endif
         if (pl.pass == 0) {  // counters and mask clear once per round, not per pass
             offered += M.count();
             winners += Me.count();
@@ -636,12 +535,9 @@ __global__ void k_pass_advance(Control* C) {
 
 constexpr int kPartThreads = 512;
 
-// dynamic shared memory of k_exact_scatter<W, false, *> (candidates_sig tables)
+// dynamic shared memory of k_exact_scatter<W, false, *> (none: K1's state lives in registers)
 template <int W>
-constexpr int scatter_smem() {
-    return W == 1 && ETWG_K1 == 3 ? sig_smem_bytes(kThreads)
-                                  : (W == 1 && ETWG_WARP_DEDUP ? kDDSlots * (kThreads / 32) * 12 : 0);
-}
+constexpr int scatter_smem() { return 0; }
 
 // BLOOM: the round's distinct keys then meet the reference's Bloom filter
 // (bit positions (h1 + i*h2) mod m, bloom.cpp:86-97), each exactly once, so
