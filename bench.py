@@ -248,8 +248,15 @@ def golden_parity(stats):
         (a["k"], a["outcome"], a["added_edges"]) == (w["k"], w["outcome"], w["added_edges"]) and
         [[l["round"], l["expanded"], l["emitted"], l["duplicates"], l["mmw_pruned"], l["overflowed"]]
          for l in a["layers"]] == w["layers"] for a, w in zip(att, g["attempts"])))
+    ref_s = sum(a.get("ref_s", 0.0) for a in g["attempts"])
     return {"golden": "tests/golden/g48_ref.json", "golden_sha256": hashlib.sha256(raw).hexdigest()[:16],
-            "rounds_compared": sum(len(w["layers"]) for w in g["attempts"]), "match": bool(match)}
+            "rounds_compared": sum(len(w["layers"]) for w in g["attempts"]), "match": bool(match),
+            # time to exact treewidth of the reference itself, recorded when the
+            # golden was generated (not timed by this run): its decide on every
+            # attempt of the same sweep
+            "reference_time_to_tw_s": round(ref_s, 1),
+            "reference_time_to_tw_hosts": "k=11..21 on 8 threads (dev container), k=22..24 on 14 threads "
+                                          "of the GPU box's 16-core host (tests/golden/make_big_goldens.py)"}
 
 
 def roofline(p):
