@@ -509,9 +509,6 @@ __device__ __forceinline__ Set<W> candidates_slots(const Set<W>* adj, int k, con
 #define ETWG_HALF_SLOTS 8
 #endif
 constexpr int kHalfSlots = ETWG_HALF_SLOTS;
-#ifndef ETWG_HALF_GUARD
-#define ETWG_HALF_GUARD 0
-#endif
 
 __device__ __forceinline__ u64 candidates_half(const Set<1>* adj, int k, u64 S, u64 eligible) {
     unsigned slo[kHalfSlots], shi[kHalfSlots];
@@ -568,9 +565,6 @@ __device__ __forceinline__ u64 candidates_half(const Set<1>* adj, int k, u64 S, 
             unsigned qlo = static_cast<unsigned>(a) & ~Slo, qhi = static_cast<unsigned>(a >> 32) & ~Shi;
 #pragma unroll
             for (int j = 0; j < kHalfSlots; ++j) {
-#if ETWG_HALF_GUARD
-                if (j >= ns) break;  // a warp whose lanes all use fewer slots skips the rest
-#endif
                 if (((h ? shi[j] : slo[j]) & bit) != 0) {
                     qlo |= slo[j];
                     qhi |= shi[j];

@@ -144,9 +144,6 @@ __device__ __forceinline__ bool halted(const Control* C) {
 #ifndef ETWG_EMIT_FLAT
 #define ETWG_EMIT_FLAT 0  // 1: children flattened over the warp's lanes; 0: each lane emits its own (-0.8 %)
 #endif
-#ifndef ETWG_PART_MULHASH
-#define ETWG_PART_MULHASH 0  // 1: bucket = top bits of key * golden-ratio constant (one multiply)
-#endif
 #ifndef ETWG_PART_TMA
 #define ETWG_PART_TMA 1  // 1: k_exact_part_tma (cp.async.bulk staging) for exact rounds of one-word keys
 #endif
@@ -293,10 +290,6 @@ __device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C,
 
 template <int W>
 __device__ __forceinline__ u64 part_of(const Set<W>& key, int lg) {
-#if ETWG_PART_MULHASH
-    if constexpr (W == 1)  // one multiply: the top bits of key * odd constant
-        return lg ? (key.w[0] * 0x9E3779B97F4A7C15ULL) >> (64 - lg) : 0;
-#endif
     return lg ? slot_hash<W>(key) >> (64 - lg) : 0;
 }
 

@@ -47,9 +47,14 @@ def init_shards(device: Optional[int] = None) -> dict:
     rank, world, local = env_rank()
     if world == 1:
         return E.shard_info()
+    dev = local if device is None else device
+    # etwg_shard_init re-binds the library's single-device engine (the
+    # replicated prefix) to this device too; the variable covers any engine
+    # use before it (the engine reads ETWG_DEVICE on first use)
+    os.environ.setdefault("ETWG_DEVICE", str(dev))
     dist = ensure_process_group()
     uid = share_unique_id(dist)
-    E.shard_init(uid, dist.get_rank(), dist.get_world_size(), local if device is None else device)
+    E.shard_init(uid, dist.get_rank(), dist.get_world_size(), dev)
     return E.shard_info()
 
 
