@@ -15,6 +15,9 @@
 
 #include "graph.hpp"
 
+#include <cstdio>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are free unless a profiler attaches
+
 namespace etw {
 
 struct DeviceError : std::runtime_error {
@@ -161,5 +164,20 @@ void shard_timer_begin();
 double shard_timer_end();
 void shard_accumulate(KernelTimes& t);
 void shard_reset_times();
+
+// NVTX range for the whole scope (solve, attempt, decide, round chunk,
+// sharded round, buffer growth): visible in ncu --nvtx / Nsight timelines.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    template <typename... A>
+    NvtxRange(const char* fmt, A... a) {
+        char buf[96];
+        std::snprintf(buf, sizeof buf, fmt, a...);
+        nvtxRangePushA(buf);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace etw

@@ -1031,6 +1031,7 @@ public:
 
     DecideResult decide(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg, int rounds,
                         const LayerObserver* observer) {
+        NvtxRange nvtx("shard decide k=%d G=%d", k, G_);
         check(cudaSetDevice(device_), "cudaSetDevice");
         const int n = g.vertex_count();
         const int W = n > 64 ? 2 : 1;
@@ -1087,6 +1088,7 @@ public:
         const int r_first = r;
         bool stopped = false;
         while (r < rounds && !stopped) {
+            NvtxRange round_range("shard round %d", r);
             Plan pl = plan(r, count, prev, cfg, W);
             pl_round_parity_ = r & 1;
             if (trace_)

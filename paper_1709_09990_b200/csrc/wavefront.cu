@@ -1240,6 +1240,7 @@ public:
     DecideResult decide(const Graph& g, int k, const HostSet& forbidden, const DpConfig& cfg,
                         int rounds, const LayerObserver* observer, u64 handoff_above = 0,
                         EngineLayer* handoff = nullptr) {
+        NvtxRange nvtx("etw decide k=%d", k);
         require_device();
         const int n = g.vertex_count();
         const int W = n > 64 ? 2 : 1;
@@ -1840,6 +1841,7 @@ private:
     }
 
     void run_rounds(int W, const DpConfig& cfg, int rounds, int k, const LayerObserver* observer) {
+        NvtxRange nvtx("rounds W=%d", W);
         if (!ensure_parts(u64{1} << 21, u64{1} << 22)) throw DeviceError("device engine: no memory for records");
         ensure_bloom(u64{1} << 22);
         ensure_claims(u64{1} << 20);
@@ -1861,6 +1863,7 @@ private:
         for (;;) {
             const int start = static_cast<int>(h_ctl_->round);
             const int end = std::min(rounds, start + chunk);
+            NvtxRange chunk_range("round chunk %d..%d", start, end - 1);
             if (epoch_ + static_cast<unsigned>(end - start) + 1 >= kEpochMask) {
                 // the device advances the epoch once per round and would wrap
                 // inside this chunk: restart the tags from a cleared state now
@@ -1912,6 +1915,7 @@ private:
 
     // Grows the structure an aborted round asked for and re-arms the round.
     void grow(Control& c, int W) {
+        NvtxRange nvtx("grow abort=%u", c.abort);
         const unsigned r = c.round;
         if (bloom_round_) {  // the aborted attempt may have set bits in filter r&1
             bloom_dirty_[r & 1] = std::max<u64>(
