@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    unsigned phase[2] = {0, 0};
+    unsigned phases = 0;  // bit st: parity of stage st's next completion (a register, not an array)
     auto count_of = [&](u64 lp) -> unsigned {
         const unsigned c = B.cursors[lp * passes + pass];
         return c < cap ? c : static_cast<unsigned>(cap);
@@ -631,8 +631,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
         const unsigned nch = (cnt + kTmaChunk - 1) / kTmaChunk;
         for (unsigned c = 0; c < nch; ++c) {
             const int st = c & 1;
-            bar_wait(bars + st, phase[st]);
-            phase[st] ^= 1;
+            bar_wait(bars + st, (phases >> st) & 1u);
+            phases ^= 1u << st;
             const unsigned n = min(cnt - c * kTmaChunk, static_cast<unsigned>(kTmaChunk));
             const u64* sb = stage + st * kTmaChunk * 2;
             for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
