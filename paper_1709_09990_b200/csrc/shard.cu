@@ -71,9 +71,6 @@ constexpr int kMaxShards = 8;
 #endif
 constexpr int kOwnerThreads = 512;
 constexpr int kRouteThreads = 256;
-#ifndef ETWG_OWNER_BATCH
-#define ETWG_OWNER_BATCH 4  // records in flight per thread in k_owner_emit
-#endif
 #ifndef ETWG_ROUTE_LANE_EMIT
 #define ETWG_ROUTE_LANE_EMIT 1  // k_route: each lane routes its own children (0: flattened over the warp)
 #endif
@@ -558,31 +555,14 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner_emit(const Params* __re
         }
         if (threadIdx.x == 0) s_full = 0;
         __syncthreads();
-        // every source's records for this partition as one flat index space
-        // (G short segments), OWNER_BATCH records in flight per thread: a loop
-        // per source left one outstanding load per thread
-        unsigned seg[kMaxShards + 1];
-        seg[0] = 0;
-        for (int s = 0; s < pl.G; ++s) seg[s + 1] = seg[s] + min(B.src_cnt[s][part], static_cast<unsigned>(pl.cap));
-        const unsigned total = seg[pl.G];
-        constexpr int kOB = ETWG_OWNER_BATCH;
-        for (unsigned base = threadIdx.x; base < total; base += kOB * blockDim.x) {
-            Set<W> keyv[kOB];
-            u64 packv[kOB];
-#pragma unroll
-            for (int j = 0; j < kOB; ++j) {
-                const unsigned f = base + j * blockDim.x;
-                if (f >= total) break;
-                int s = 0;
-                while (f >= seg[s + 1]) ++s;
-                const u64* rec = B.src_recs[s] + (part * pl.cap + (f - seg[s])) * srec_words<W>();
-                load_srec<W>(rec, keyv[j], packv[j]);
-                packv[j] |= static_cast<u64>((s - pl.me + pl.G) % pl.G) << 40;  // emitter priority
-            }
-#pragma unroll
-            for (int j = 0; j < kOB; ++j) {
-                if (base + j * blockDim.x >= total) break;
-                const Set<W>& key = keyv[j];
+        for (int s = 0; s < pl.G; ++s) {
+            const u64 pri = static_cast<u64>((s - pl.me + pl.G) % pl.G) << 40;
+            const unsigned cnt = min(B.src_cnt[s][part], static_cast<unsigned>(pl.cap));
+            const u64* recs = B.src_recs[s] + part * pl.cap * srec_words<W>();
+            for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
+                Set<W> key;
+                u64 packed;
+                load_srec<W>(recs + static_cast<u64>(i) * srec_words<W>(), key, packed);
                 unsigned h = static_cast<unsigned>(slot_hash<W>(key)) & (SLOTS - 1);
                 bool placed = false;
                 for (int probe = 0; probe < SLOTS && !placed; ++probe) {
@@ -590,12 +570,12 @@ __global__ void __launch_bounds__(kOwnerThreads) k_owner_emit(const Params* __re
                     if (!placed) h = (h + 1) & (SLOTS - 1);
                 }
                 if (placed) {
-                    const u64 mine = packv[j];  // ranks only decrease: skip the atomic when already beaten
+                    const u64 mine = pri | packed;  // ranks only decrease: skip the atomic when already beaten
                     if (!ETWG_CLAIM_PEEK || mine < *reinterpret_cast<volatile u64*>(ranks + h))
                         atomicMin(reinterpret_cast<unsigned long long*>(ranks + h), mine);
-                } else {
-                    s_full = 1;
                 }
+                else
+                    s_full = 1;
             }
         }
         __syncthreads();
