@@ -439,6 +439,10 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
             if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
         }
         bool full = false;
+        // ETWG_DEBUG 16384 (diagnostics only, results invalid): the decide's
+        // last round evaluates its candidates but emits no records — times K1
+        // without the bucket scatter
+        if ((P->flags & 16384) && static_cast<int>(r) + 1 == P->rounds) continue;
 #if ETWG_EMIT_FLAT == 0
         // each lane emits its own parent's children, two per step so both
         // bucket-cursor atomics are in flight together; no flattening
