@@ -322,6 +322,66 @@ __device__ __forceinline__ void record_store(const Bufs& B, const PartPlan& pl, 
 }
 
 
+// Emission of one parent's children by its own lane (the default scatter
+// emission): two bucket-cursor atomics in flight per lane, one 16-byte record
+// per child, `full` set when a bucket is out of room.
+template <int W>
+__device__ __forceinline__ void emit_lane(const Bufs& B, const PartPlan& pl, int n, const Set<W>& S,
+                                          const Set<W>& M, u64 idx, bool& full) {
+    Set<W> rest = M;
+    constexpr int LU = ETWG_LANE_UNROLL;
+    while (rest.any()) {
+        Set<W> key[LU];
+        u64 part[LU], low[LU];
+        int vv[LU];
+        unsigned slot[LU];
+#pragma unroll
+        for (int u = 0; u < LU; ++u) slot[u] = ~0u;
+#pragma unroll
+        for (int u = 0; u < LU; ++u) {
+            if (!rest.any()) break;
+            vv[u] = pop_any(rest);
+            key[u] = S;
+            key[u].add(vv[u]);
+            part[u] = record_part<W>(key[u], pl, n, low[u]);
+            if (pl.mine(part[u])) slot[u] = atomicAdd(B.cursors + part[u], 1u);
+        }
+#pragma unroll
+        for (int u = 0; u < LU; ++u) {
+            if (slot[u] == ~0u) continue;
+            if (slot[u] < pl.cap)
+                record_store<W>(B, pl, part[u], slot[u], key[u], low[u], idx, vv[u]);
+            else
+                full = true;
+        }
+    }
+}
+
+// mbarrier helpers (shared::cta) for the warp-specialised scatter
+__device__ __forceinline__ void mbar_init(u64* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WSWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WSWAIT_%=;\n\t}" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+        "r"(parity)
+        : "memory");
+}
+
+#ifndef ETWG_WS
+#define ETWG_WS 1  // warp-specialised scatter: K1 warps feed emission warps through shared memory
+#endif
+constexpr int kWsPairs = kThreads / 64;  // producer / consumer warp pairs per CTA
+
 #ifndef ETWG_SCATTER_MINB
 #define ETWG_SCATTER_MINB 0  // >0: ask ptxas for that many resident CTAs per SM (register cap)
 #endif
@@ -391,6 +451,73 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     // Small layer (fewer than 1/8 of the resident threads): one warp per
     // parent, candidates and MMW bounds spread over the lanes.
     const bool small = (P->flags & 256) || (!(P->flags & 128) && E * 8 <= static_cast<u64>(gridDim.x) * blockDim.x);
+    if (ETWG_WS && W == 1 && !MMW && !small) {
+        // Warp specialisation (measured: K1 alone is ~46 % of this kernel,
+        // the bucket scatter the rest, and in one warp they serialise). Warp
+        // w < kWsPairs is a producer: K1 for 32 consecutive parents, then
+        // (S, child mask) into its pair's double-buffered shared slot;
+        // warp w + kWsPairs is its consumer: takes the slot, releases it and
+        // emits the children (atomics + stores) while the producer already
+        // evaluates the next 32 parents. full/empty handshakes on mbarriers.
+        __shared__ u64 ws_S[kWsPairs][2][32], ws_M[kWsPairs][2][32], ws_base[kWsPairs][2];
+        __shared__ __align__(8) u64 ws_bar[kWsPairs][2][2];  // [pair][buffer][full, empty]
+        const int warp = threadIdx.x >> 5;
+        const int pair = warp % kWsPairs;
+        if (threadIdx.x < kWsPairs * 4) mbar_init(&ws_bar[threadIdx.x >> 2][(threadIdx.x >> 1) & 1][threadIdx.x & 1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncthreads();
+        const u64 producers = static_cast<u64>(gridDim.x) * kWsPairs;
+        const u64 me = static_cast<u64>(blockIdx.x) * kWsPairs + pair;
+        if (warp < kWsPairs) {
+            for (unsigned it = 0;; ++it) {
+                const int b = it & 1;
+                if (it >= 2) mbar_wait(&ws_bar[pair][b][1], ((it >> 1) - 1) & 1u);  // consumer released it
+                const u64 base = (me + it * producers) * 32;
+                const bool done = base >= E || *reinterpret_cast<volatile unsigned*>(&C->abort) != 0;
+                if (done) {
+                    if (lane == 0) {
+                        ws_base[pair][b] = ~u64{0};
+                        mbar_arrive(&ws_bar[pair][b][0]);
+                    }
+                    break;
+                }
+                const u64 idx = base + lane;
+                const bool valid = idx < E;
+                const Set<W> S = valid ? load_set<W>(in, idx) : Set<W>::zero();
+                const Set<W> M =
+                    warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
+                if (pl.pass == 0) {
+                    offered += M.count();
+                    winners += M.count();
+                    if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
+                }
+                ws_S[pair][b][lane] = S.w[0];
+                ws_M[pair][b][lane] = M.w[0];
+                if (lane == 0) ws_base[pair][b] = base;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ws_bar[pair][b][0]);
+            }
+        } else {
+            const bool k1_only = (P->flags & 16384) && static_cast<int>(r) + 1 == P->rounds;  // diagnostics
+            for (unsigned it = 0;; ++it) {
+                const int b = it & 1;
+                mbar_wait(&ws_bar[pair][b][0], (it >> 1) & 1u);
+                const u64 base = ws_base[pair][b];
+                if (base == ~u64{0}) break;
+                Set<W> S, M;
+                S.w[0] = ws_S[pair][b][lane];
+                M.w[0] = ws_M[pair][b][lane];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ws_bar[pair][b][1]);
+                bool full = false;
+                if (!k1_only) emit_lane<W>(B, pl, n, S, M, base + lane, full);
+                if (__any_sync(kFull, full) && lane == 0) {
+                    C->need = 2 * pl.cap;
+                    C->abort = kGrowRecs;
+                }
+            }
+        }
+    } else
     if (small) {  // ETWG_DEBUG 128 / 256 force the thread / warp mode (tests)
         Set<W>* R = warp_tables[threadIdx.x >> 5][0];
         Set<W>* rows = warp_tables[threadIdx.x >> 5][MMW ? 1 : 0];
@@ -444,38 +571,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         // without the bucket scatter
         if ((P->flags & 16384) && static_cast<int>(r) + 1 == P->rounds) continue;
 #if ETWG_EMIT_FLAT == 0
-        // each lane emits its own parent's children, two per step so both
-        // bucket-cursor atomics are in flight together; no flattening
-        // shuffles (the trip count is the warp's largest child count)
-        {
-            Set<W> rest = Me;
-            constexpr int LU = ETWG_LANE_UNROLL;
-            while (rest.any()) {
-                Set<W> key[LU];
-                u64 part[LU], low[LU];
-                int vv[LU];
-                unsigned slot[LU];
-#pragma unroll
-                for (int u = 0; u < LU; ++u) slot[u] = ~0u;
-#pragma unroll
-                for (int u = 0; u < LU; ++u) {
-                    if (!rest.any()) break;
-                    vv[u] = pop_any(rest);
-                    key[u] = S;
-                    key[u].add(vv[u]);
-                    part[u] = record_part<W>(key[u], pl, n, low[u]);
-                    if (pl.mine(part[u])) slot[u] = atomicAdd(B.cursors + part[u], 1u);
-                }
-#pragma unroll
-                for (int u = 0; u < LU; ++u) {
-                    if (slot[u] == ~0u) continue;
-                    if (slot[u] < pl.cap)
-                        record_store<W>(B, pl, part[u], slot[u], key[u], low[u], idx, vv[u]);
-                    else
-                        full = true;
-                }
-            }
-        }
+        emit_lane<W>(B, pl, n, S, Me, idx, full);
 #else
         WarpFlat f;
         f.scan(M.count());
