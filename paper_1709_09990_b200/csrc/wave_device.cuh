@@ -30,6 +30,7 @@ using u64 = unsigned long long;
 struct Params {
     int n, k, rounds, free_count;
     int hashes, bpe, any_pop, flags;  // flags: ETWG_DEBUG bits (tests only)
+    int gtab, pad_;                   // >0: exact rounds whose table fits 2^gtab slots dedup in a global table
     u64 max_states;
     u64 forbidden[2];
     u64 rows[kMaxVertices][2];

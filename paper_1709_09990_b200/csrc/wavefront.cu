@@ -63,6 +63,7 @@ struct RoundStats {
     u64 fp;       // partitioned Bloom: of those, rejected by the filter (false positives)
     unsigned overflowed, valid;
     unsigned compact, nb;  // exact mode: 8-byte records this round (PartPlan)
+    unsigned gtab, pad4;   // exact mode: global-table round (PartPlan::gtab; pcap = table slots)
 };
 
 enum AbortCode : unsigned {
@@ -73,6 +74,7 @@ enum AbortCode : unsigned {
     kGrowParts = 5,    // a partition's distinct keys overflowed its shared table
     kGrowRecs = 6,     // a partition's records overflowed its capacity
     kGrowPartBuf = 7,  // record buffer / cursor array too small for the plan
+    kGrowTable = 8,    // a global-table probe chain ran out (raise tab_floor)
 };
 
 struct Control {
@@ -88,6 +90,7 @@ struct Control {
     unsigned handed, pad2;
     u64 part_floor;     // exact mode: minimum partitions after a grow (per decide)
     u64 rec_floor;      // exact mode: minimum records per partition after a grow
+    u64 tab_floor;      // exact mode: minimum global-table slots after a probe overflow
     unsigned passes;    // exact mode: hash-range passes per round (host-set, >= 1)
     unsigned pass;      // current pass of the round (k_pass_advance; reset by the append)
     unsigned fp_log_n;  // ETWG_DEBUG 2048: first false positives logged (key, h1, h2, m)
@@ -111,7 +114,18 @@ struct Bufs {
     u64 bloom_cap;   // 32-bit words
     u64* claims;     // Bloom-mode claim table, 16-byte {key, epoch} slots
     u64 claim_cap;   // slots
+    u64* tab;        // exact mode: global {key, ~min rank} table (empty between rounds)
+    u64 tab_cap;     // slots
 };
+
+// Bucket cursors sit kCursorStride words apart: the L2's atomic unit
+// serialises atomics to one cache line, and ~200 K cursors packed 32 per
+// 128-byte line put ten-odd thousand emissions per round behind each line.
+#ifndef ETWG_CURSOR_STRIDE
+#define ETWG_CURSOR_STRIDE 1
+#endif
+constexpr u64 kCursorStride = ETWG_CURSOR_STRIDE;
+__device__ __forceinline__ unsigned* cursor_at(const Bufs& B, u64 part) { return B.cursors + part * kCursorStride; }
 
 __device__ __forceinline__ bool halted(const Control* C) {
     return (*reinterpret_cast<const volatile unsigned*>(&C->stop) |
@@ -236,12 +250,19 @@ struct PartPlan {
     // pass only are held, so the record buffer is np/passes * cap.
     unsigned passes, pass;
     int lgp;  // log2(passes)
+    // Global-table rounds (exact, one-word keys, the round's table fits
+    // 2^P->gtab slots, i.e. stays L2-resident): no buckets; every child goes
+    // straight into an open-addressing {key, ~min rank} table of `cap` slots
+    // (a power of two) in B.tab; np = passes, so `part` is only the pass
+    // selector. Larger rounds keep the bucket records: random 16-byte probes
+    // into a multi-GB table measured 1.59 s vs 1.03 s per G(48,0.2) solve.
+    int gtab;
     __device__ __forceinline__ bool mine(u64 part) const { return (part & (passes - 1)) == pass; }
     __device__ __forceinline__ u64 local(u64 part) const { return part >> lgp; }
 };
 
 template <int W>
-__device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C, unsigned r, u64 E) {
+__device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C, unsigned r, u64 E, u64 B_tab_cap) {
     const u64 upper = E * static_cast<u64>(P->free_count > 0 ? P->free_count : 1);
     u64 distinct = upper, winners = upper;
     if (r > 0 && C->rs[r - 1].expanded) {
@@ -282,6 +303,25 @@ __device__ __forceinline__ PartPlan part_plan(const Params* P, const Control* C,
         if (pl.compact) pl.nb = P->n - pl.lg;
     }
     pl.lgp = __ffs(static_cast<int>(pl.passes)) - 1;
+    pl.gtab = 0;
+    if (W == 1 && P->gtab) {
+        // load factor <= 1/2 on the planned distinct keys of this pass; a
+        // probe chain past kTabProbes aborts the round and raises tab_floor
+        const u64 per_pass = (distinct + pl.passes - 1) / pl.passes;
+        u64 t = ceil_pow2(2 * per_pass);
+        if (tight) t = t > 256 ? t / 16 : 16;
+        if (t < 16) t = 16;
+        while (t < C->tab_floor) t <<= 1;
+        if (t <= (u64{1} << P->gtab) && t <= B_tab_cap) {
+            pl.gtab = 1;
+            pl.compact = 0;
+            pl.nb = 0;
+            pl.np = pl.passes;
+            pl.lg = pl.lgp;
+            pl.cap = t;
+            return pl;
+        }
+    }
     const u64 per = (winners + pl.np - 1) / pl.np;
     pl.cap = tight ? per / 4 + 1 : per + per / 4 + 64;
     if (pl.cap < C->rec_floor) pl.cap = C->rec_floor;
@@ -344,7 +384,7 @@ __device__ __forceinline__ void emit_lane(const Bufs& B, const PartPlan& pl, int
             key[u] = S;
             key[u].add(vv[u]);
             part[u] = record_part<W>(key[u], pl, n, low[u]);
-            if (pl.mine(part[u])) slot[u] = atomicAdd(B.cursors + part[u], 1u);
+            if (pl.mine(part[u])) slot[u] = atomicAdd(cursor_at(B, part[u]), 1u);
         }
 #pragma unroll
         for (int u = 0; u < LU; ++u) {
@@ -354,6 +394,72 @@ __device__ __forceinline__ void emit_lane(const Bufs& B, const PartPlan& pl, int
             else
                 full = true;
         }
+    }
+}
+
+// Global-table emission (PartPlan::gtab): slot = {key, ~rank}, key 0 =
+// empty (a child is never the empty set), the inverted rank so that an
+// all-zero slot is "no rank yet" and the minimum rank is an atomicMax.
+// Linear probing from slot_hash & (cap-1); a 32-byte sector holds two slots.
+// The first slot of each of ETWG_TAB_UNROLL children is loaded (L2 only)
+// before any is resolved, so the lane has that many random reads in flight;
+// a slot that already holds the key with a lower rank costs no atomic.
+#ifndef ETWG_TAB_UNROLL
+#define ETWG_TAB_UNROLL 2  // 4: 127 registers (80 at 2), slower
+#endif
+#ifndef ETWG_GTAB_LG
+#define ETWG_GTAB_LG 22  // global table up to 2^22 slots = 64 MB (L2 is 126 MB)
+#endif
+constexpr int kGtabLg = ETWG_GTAB_LG;
+constexpr int kTabProbes = 64;
+
+__device__ __forceinline__ void tab_settle(ulonglong2* tab, u64 mask, u64 key, u64 inv, u64 s, ulonglong2 cur,
+                                           bool& full) {
+    for (int p = 0;;) {
+        u64 k = cur.x;
+        if (k == 0) {
+            k = atomicCAS(reinterpret_cast<unsigned long long*>(&tab[s].x), 0ull, key);
+            if (k == 0) k = key;
+        }
+        if (k == key) {
+            if (cur.y < inv) atomicMax(reinterpret_cast<unsigned long long*>(&tab[s].y), inv);
+            return;
+        }
+        if (++p == kTabProbes) {
+            full = true;
+            return;
+        }
+        s = (s + 1) & mask;
+        cur = __ldcg(tab + s);
+    }
+}
+
+__device__ __forceinline__ void emit_lane_tab(const Bufs& B, const PartPlan& pl, u64 S, u64 M, u64 idx,
+                                              bool& full) {
+    ulonglong2* tab = reinterpret_cast<ulonglong2*>(B.tab);
+    const u64 mask = pl.cap - 1;
+    constexpr int LU = ETWG_TAB_UNROLL;
+    while (M) {
+        u64 key[LU], inv[LU], s[LU];
+        ulonglong2 cur[LU];
+        bool act[LU];
+#pragma unroll
+        for (int u = 0; u < LU; ++u) {
+            act[u] = false;
+            if (!M) continue;
+            const int v = __ffsll(static_cast<long long>(M)) - 1;
+            M &= M - 1;
+            key[u] = S | (u64{1} << v);
+            const u64 h = fmix64(key[u]);  // slot_hash<1>
+            if (!pl.mine(pl.lg ? h >> (64 - pl.lg) : 0)) continue;
+            act[u] = true;
+            inv[u] = ~child_rank<1>(idx, v);
+            s[u] = h & mask;
+            cur[u] = __ldcg(tab + s[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < LU; ++u)
+            if (act[u]) tab_settle(tab, mask, key[u], inv[u], s[u], cur[u], full);
     }
 }
 
@@ -401,8 +507,8 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     if (halted(C)) return;
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
-    const PartPlan pl = part_plan<W>(P, C, r, E);
-    const u64 rec_need = (pl.np >> pl.lgp) * pl.cap * (W == 1 && pl.compact ? 1 : rec_words<W>());  // u64 words
+    const PartPlan pl = part_plan<W>(P, C, r, E, B.tab_cap);
+    const u64 rec_need = pl.gtab ? 0 : (pl.np >> pl.lgp) * pl.cap * (W == 1 && pl.compact ? 1 : rec_words<W>());  // u64 words
     if (pl.np > B.cursor_cap || rec_need > B.rec_cap) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             C->need = rec_need;
@@ -437,6 +543,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         C->rs[r].pcap = pl.cap;
         C->rs[r].compact = pl.compact;
         C->rs[r].nb = pl.nb;
+        C->rs[r].gtab = pl.gtab;
     }
     const int n = P->n;
     const int lane = threadIdx.x & 31;
@@ -510,10 +617,15 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ws_bar[pair][b][1]);
                 bool full = false;
-                if (!k1_only) emit_lane<W>(B, pl, n, S, M, base + lane, full);
+                if (k1_only) {
+                } else if (pl.gtab) {
+                    emit_lane_tab(B, pl, S.w[0], M.w[0], base + lane, full);
+                } else {
+                    emit_lane<W>(B, pl, n, S, M, base + lane, full);
+                }
                 if (__any_sync(kFull, full) && lane == 0) {
                     C->need = 2 * pl.cap;
-                    C->abort = kGrowRecs;
+                    C->abort = pl.gtab ? kGrowTable : kGrowRecs;
                 }
             }
         }
@@ -537,9 +649,13 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 Set<W> key = S;
                 key.add(v);
                 u64 low;
+                if (W == 1 && pl.gtab) {
+                    emit_lane_tab(B, pl, S.w[0], key.w[0] ^ S.w[0], p, full);
+                    continue;
+                }
                 const u64 part = record_part<W>(key, pl, n, low);
                 if (!pl.mine(part)) continue;
-                const unsigned slot = atomicAdd(B.cursors + part, 1u);
+                const unsigned slot = atomicAdd(cursor_at(B, part), 1u);
                 if (slot < pl.cap)
                     record_store<W>(B, pl, part, slot, key, low, p, v);
                 else
@@ -548,7 +664,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         }
         if (__any_sync(kFull, full) && lane == 0) {
             C->need = 2 * pl.cap;
-            C->abort = kGrowRecs;
+            C->abort = pl.gtab ? kGrowTable : kGrowRecs;
         }
     } else
     for (u64 base = ((blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5) * 32; base < E;
@@ -570,6 +686,9 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         // last round evaluates its candidates but emits no records — times K1
         // without the bucket scatter
         if ((P->flags & 16384) && static_cast<int>(r) + 1 == P->rounds) continue;
+        if (W == 1 && pl.gtab) {
+            emit_lane_tab(B, pl, S.w[0], Me.w[0], idx, full);
+        } else {
 #if ETWG_EMIT_FLAT == 0
         emit_lane<W>(B, pl, n, S, Me, idx, full);
 #else
@@ -596,7 +715,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                     vv[u] = nth_member<W>(Ms, j - excl);
                     key[u].add(vv[u]);
                     part[u] = record_part<W>(key[u], pl, n, low[u]);
-                    if (pl.mine(part[u])) slot[u] = atomicAdd(B.cursors + part[u], 1u);
+                    if (pl.mine(part[u])) slot[u] = atomicAdd(cursor_at(B, part[u]), 1u);
                 }
             }
 #pragma unroll
@@ -609,9 +728,10 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
             }
         }
 #endif
+        }
         if (__any_sync(kFull, full) && lane == 0) {
             C->need = 2 * pl.cap;
-            C->abort = kGrowRecs;
+            C->abort = pl.gtab ? kGrowTable : kGrowRecs;
         }
     }
 #pragma unroll
@@ -689,7 +809,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
     __shared__ unsigned s_full;
     if (halted(C)) return;
     const unsigned r = C->round;
-    if (C->rs[r].compact) return;
+    if (C->rs[r].compact || C->rs[r].gtab) return;
     const u64 passes = C->passes ? C->passes : 1;
     const u64 pass = C->pass;
     const u64 np = C->rs[r].np / passes;
@@ -703,7 +823,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
     __syncthreads();
     unsigned phases = 0;  // bit st: parity of stage st's next completion (a register, not an array)
     auto count_of = [&](u64 lp) -> unsigned {
-        const unsigned c = B.cursors[lp * passes + pass];
+        const unsigned c = *cursor_at(B, lp * passes + pass);
         return c < cap ? c : static_cast<unsigned>(cap);
     };
     // issues chunks [c0, c0+k) of local bucket lp into their stages (thread 0)
@@ -785,13 +905,32 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
             const int v = static_cast<int>(rank % 64);
             atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + parent, u64{1} << v);
         }
-        if (threadIdx.x == 0) B.cursors[part] = 0;
+        if (threadIdx.x == 0) *cursor_at(B, part) = 0;
         __syncthreads();
     }
     if (BLOOM) {
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) probed += __shfl_xor_sync(kFull, probed, o);
         if ((threadIdx.x & 31) == 0 && probed) atomicAdd(&C->rs[r].probed, probed);
+    }
+}
+
+// Global-table rounds: one streaming pass over the pass's table marks each
+// key's min-rank child in its parent's winner mask (what k_exact_part does
+// per bucket) and leaves every slot empty for the next round / pass.
+__global__ void __launch_bounds__(kThreads) k_tab_mark(Control* C, Bufs B) {
+    if (halted(C)) return;
+    const unsigned r = C->round;
+    if (!C->rs[r].gtab) return;  // a bucket round: k_exact_part* runs it
+    const u64 slots = C->rs[r].pcap;
+    ulonglong2* tab = reinterpret_cast<ulonglong2*>(B.tab);
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < slots; i += stride) {
+        const ulonglong2 e = __ldcs(tab + i);
+        if (e.x == 0) continue;
+        const u64 rank = ~e.y;
+        atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + rank / 64, u64{1} << (rank % 64));
+        tab[i] = make_ulonglong2(0, 0);
     }
 }
 
@@ -804,7 +943,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
     __shared__ unsigned s_full;
     if (halted(C)) return;
     const unsigned r = C->round;
-    if (W == 1 && C->rs[r].compact) return;  // k_exact_part_compact's round
+    if (W == 1 && (C->rs[r].compact || C->rs[r].gtab)) return;  // k_exact_part_compact's / k_tab_mark's round
     const u64 passes = C->passes ? C->passes : 1;
     const u64 pass = C->pass;
     const u64 np = C->rs[r].np / passes;  // this pass's buckets: part = lp * passes + pass
@@ -816,7 +955,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
         for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) ranks[i] = ~u64{0};
         if (threadIdx.x == 0) s_full = 0;
         __syncthreads();
-        const unsigned cnt = B.cursors[part];
+        const unsigned cnt = *cursor_at(B, part);
         const u64* recs = B.recs + lp * cap * rec_words<W>();
         // PART_BATCH records in flight per thread before any probing: one
         // outstanding 16 B load per thread cannot cover HBM latency at the
@@ -901,7 +1040,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
             const int v = static_cast<int>(rank % (64 * W));
             atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + parent * W + (v >> 6), u64{1} << (v & 63));
         }
-        if (threadIdx.x == 0) B.cursors[part] = 0;  // clean for the next round
+        if (threadIdx.x == 0) *cursor_at(B, part) = 0;  // clean for the next round
         __syncthreads();
     }
     if (BLOOM) {
@@ -943,7 +1082,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Param
         }
         if (threadIdx.x == 0) s_full = 0;
         __syncthreads();
-        const unsigned cnt = B.cursors[part];
+        const unsigned cnt = *cursor_at(B, part);
         const u64* recs = B.recs + lp * cap;
         constexpr int kBatch = 2 * ETWG_PART_BATCH;  // 8-byte records: twice as many in flight
         for (unsigned base = threadIdx.x; base < cnt; base += kBatch * blockDim.x) {
@@ -1015,7 +1154,7 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part_compact(const Param
             const u64 bit = key & ~__ldg(layer + parent);  // the one vertex the parent lacks
             atomicOr(reinterpret_cast<unsigned long long*>(B.cmask) + parent, bit);
         }
-        if (threadIdx.x == 0) B.cursors[part] = 0;  // clean for the next round
+        if (threadIdx.x == 0) *cursor_at(B, part) = 0;  // clean for the next round
         __syncthreads();
     }
     if (BLOOM) {
@@ -1470,6 +1609,9 @@ public:
         cudaFree(b_.recs);
         cudaFree(b_.cursors);
         cudaFree(b_.claims);
+        cudaFree(b_.tab);
+        b_.tab = nullptr;
+        b_.tab_cap = 0;
         b_.cmask = nullptr;
         b_.tiles = nullptr;
         b_.recs = nullptr;
@@ -1541,6 +1683,7 @@ private:
     int grid_tma_ = 0;
     bool compact_possible_ = false;  // ETWG_COMPACT build or ETWG_DEBUG 8192 this decide
     unsigned passes_ = 1;            // hash-range passes per round (f4: records beyond HBM)
+    bool gtab_ = false;              // this decide's small exact rounds may use the global table (W == 1)
     bool part_bloom_ = false;  // Bloom rounds of this decide use scatter/part/append
 
     // Epochs tag look-back statuses (24 bits); on wrap-around the status
@@ -1720,6 +1863,12 @@ private:
         p.bpe = cfg.bloom_bits_per_element;
         p.any_pop = any_pop;
         if (const char* dbg = std::getenv("ETWG_DEBUG")) p.flags = std::atoi(dbg);
+        // exact rounds of one-word keys: global open-addressing table (default)
+        // or bucket records + per-bucket shared-memory tables (ETWG_GTAB=0)
+        // ETWG_GTAB=0: every round on buckets; ETWG_GTAB=L: tables up to 2^L slots
+        const char* gt = std::getenv("ETWG_GTAB");
+        const int lg = gt ? std::atoi(gt) : kGtabLg;
+        p.gtab = cfg.dedup == DedupMode::exact_set ? std::max(0, std::min(lg, 30)) : 0;
         p.max_states = cfg.max_layer_states;
         p.forbidden[0] = forbidden.w[0];
         p.forbidden[1] = forbidden.w[1];
@@ -1804,15 +1953,30 @@ private:
         if (parts > b_.cursor_cap || !b_.cursors) {
             const u64 cap = std::max<u64>(parts, u64{1} << 16);
             if (b_.cursors) cudaFree(b_.cursors);
-            check(cudaMalloc(&b_.cursors, cap * 4), "cursors");
-            check(cudaMemsetAsync(b_.cursors, 0, cap * 4, stream_), "cursors zero");
+            check(cudaMalloc(&b_.cursors, cap * 4 * kCursorStride), "cursors");
+            check(cudaMemsetAsync(b_.cursors, 0, cap * 4 * kCursorStride, stream_), "cursors zero");
             b_.cursor_cap = cap;
         }
         return true;
     }
 
     void clean_cursors() {
-        check(cudaMemsetAsync(b_.cursors, 0, b_.cursor_cap * 4, stream_), "cursors clean");
+        check(cudaMemsetAsync(b_.cursors, 0, b_.cursor_cap * 4 * kCursorStride, stream_), "cursors clean");
+    }
+
+    // Global table: allocated once at its maximum (2^gtab slots, L2-sized),
+    // empty between rounds (k_tab_mark clears what it marks); an aborted
+    // global-table round leaves `slots` slots to clear.
+    void ensure_tab(u64 slots) {
+        if (b_.tab && b_.tab_cap >= slots) return;
+        if (b_.tab) cudaFree(b_.tab);
+        check(cudaMalloc(&b_.tab, slots * 16), "global table");
+        check(cudaMemsetAsync(b_.tab, 0, slots * 16, stream_), "global table zero");
+        b_.tab_cap = slots;
+    }
+    void clean_table(u64 slots) {
+        if (b_.tab && slots)
+            check(cudaMemsetAsync(b_.tab, 0, std::min(slots, b_.tab_cap) * 16, stream_), "table clean");
     }
 
     void ensure_bloom(u64 words) {
@@ -1909,6 +2073,10 @@ private:
             else
                 timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.expand_ms, prof.t.expand_launches);
+            // the scatter's plan picks the round's dedup; the other kernels return at once
+            if (W == 1 && gtab_ && !BLOOM)
+                timed_launch([&] { k_tab_mark<<<grid_, kThreads, 0, stream_>>>(d_ctl_, b_); },
+                             prof.t.insert_ms, prof.t.insert_launches);
             if (W == 1 && ETWG_PART_TMA && !BLOOM)  // Bloom probes want the 3-CTA kernel's warps
                 timed_launch([&] { k_exact_part_tma<BLOOM><<<grid_tma_, kTmaThreads, tma_part_smem_bytes(), stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.insert_ms, prof.t.insert_launches);
@@ -1956,6 +2124,8 @@ private:
                        cfg.use_mmw) &&
                       !(h_params_->flags & 64);
         if (bloom_round_) clean_blooms();
+        gtab_ = W == 1 && h_params_->gtab > 0;
+        if (gtab_) ensure_tab(u64{1} << h_params_->gtab);
         if (!prof.on) check(cudaEventRecord(ev_[0], stream_), "event");
         auto t0 = std::chrono::steady_clock::now();
         const bool sync_each = (h_params_->flags & 8) != 0;
@@ -2017,6 +2187,7 @@ private:
     void grow(Control& c, int W) {
         NvtxRange nvtx("grow abort=%u", c.abort);
         const unsigned r = c.round;
+        const u64 tab_dirty = gtab_ && c.rs[r].gtab ? c.rs[r].pcap : 0;  // inserts of the aborted round
         if (bloom_round_) {  // the aborted attempt may have set bits in filter r&1
             bloom_dirty_[r & 1] = std::max<u64>(
                 bloom_dirty_[r & 1], bloom_bits_for(host_round_cap(c.count[r & 1]), h_params_->bpe) / 32 + 1);
@@ -2061,6 +2232,9 @@ private:
             case kGrowBloom:
                 ensure_bloom(c.need + c.need / 4);
                 break;
+            case kGrowTable:  // beyond 2^gtab slots the plan falls back to buckets
+                c.tab_floor = std::max<u64>(c.tab_floor, c.need);
+                break;
             case kGrowClaims:
                 ensure_claims(c.need);
                 break;
@@ -2068,6 +2242,7 @@ private:
                 throw DeviceError("device engine: unknown abort code");
         }
         if (bloom_round_) clean_blooms();
+        clean_table(tab_dirty);
         // re-arm: clear the abort and the partial statistics of round r
         c.abort = kOk;
         c.need = 0;
@@ -2124,6 +2299,15 @@ private:
             if (bloom) {
                 // k_bloom_dedup: parent read + novel-mask write + h probe words per child
                 prof.t.insert_bytes += 2 * sb * E + db * P;
+            } else if (W == 1 && s.round >= 0 && s.round < kMaxRounds && h_ctl_->rs[s.round].gtab) {
+                // global table: k_exact_scatter reads the parent, clears its
+                // winner mask, reads one 16-byte slot per offered child and
+                // writes one per distinct key; k_tab_mark streams the table
+                // (pcap slots), clears each used slot, ORs the winner's bit
+                const double slots = s.round >= 0 && s.round < kMaxRounds
+                                         ? static_cast<double>(h_ctl_->rs[s.round].pcap) : 0.0;
+                prof.t.expand_bytes += 2 * sb * E + 16.0 * P + 16.0 * U;
+                prof.t.insert_bytes += 16.0 * slots + 16.0 * U + 8.0 * U;
             } else {
                 // k_exact_scatter: parent read, winner-mask clear, one record per child;
                 // k_exact_part: record read, one winner-mask OR per distinct key

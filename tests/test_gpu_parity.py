@@ -334,6 +334,21 @@ def test_hash_range_passes_agree(gpu):
     assert one == _run_with_env({"ETWG_PASSES": "2", "ETWG_DEBUG": "8192"}, _TIGHT_CODE)
 
 
+def test_global_table_equals_buckets(gpu):
+    """Exact rounds of one-word keys dedup in one global open-addressing
+    table (default) instead of bucket records + per-bucket shared tables
+    (ETWG_GTAB=0). Both keep each key's minimum emission rank, so layers,
+    histories and every counter are identical — also with undersized tables
+    (ETWG_DEBUG 1024: probe-chain overflow aborts and re-runs), several
+    hash-range passes, and the warp-per-parent scatter (ETWG_DEBUG 256)."""
+    buckets = _run_with_env({"ETWG_GTAB": "0"}, _TIGHT_CODE)
+    assert buckets == _run_with_env({}, _TIGHT_CODE)
+    assert buckets == _run_with_env({"ETWG_DEBUG": "1024"}, _TIGHT_CODE)
+    assert buckets == _run_with_env({"ETWG_PASSES": "4", "ETWG_DEBUG": "1024"}, _TIGHT_CODE)
+    assert buckets == _run_with_env({"ETWG_DEBUG": "256"}, _TIGHT_CODE)
+    assert buckets == _run_with_env({"ETWG_DEBUG": "128"}, _TIGHT_CODE)
+
+
 def _run_with_debug(flags, code):
     """Runs `code` in a fresh interpreter with ETWG_DEBUG=flags (the engine
     reads it when a decide starts) and returns its JSON output."""

@@ -22,6 +22,11 @@ alg = {  # W = 1 (n <= 64) exact mode, bytes per launch
     "k_append": 20 * E + 12 * U,
     "k_route": 8 * E + 16 * P,
     "k_owner": 16 * P + 12 * U,
+    # global-table rounds (default for one-word exact rounds): one 16-byte
+    # slot read per offered child, one slot written per distinct key; the
+    # mark pass streams the table (TAB_SLOTS slots, from the decide's trace)
+    "k_exact_scatter@gtab": 16 * E + 16 * P + 16 * U,
+    "k_tab_mark": 16 * int(__import__("os").environ.get("TAB_SLOTS", "0")) + 24 * U,
 }
 
 
