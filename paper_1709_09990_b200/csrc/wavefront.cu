@@ -486,7 +486,13 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
 #ifndef ETWG_WS
 #define ETWG_WS 1  // warp-specialised scatter: K1 warps feed emission warps through shared memory
 #endif
-constexpr int kWsPairs = kThreads / 64;  // producer / consumer warp pairs per CTA
+#ifndef ETWG_WS_PROD
+#define ETWG_WS_PROD 4  // producer warps per CTA; the other warps consume, kWsCpp per producer
+#endif
+constexpr int kWsProd = ETWG_WS_PROD;
+constexpr int kWsCpp = (kThreads / 32 - kWsProd) / kWsProd;  // consumer warps per producer
+constexpr int kWsRing = 2 * kWsCpp;                           // shared slots per producer
+static_assert(kWsProd * (1 + kWsCpp) == kThreads / 32, "warp roles must fill the CTA");
 
 #ifndef ETWG_SCATTER_MINB
 #define ETWG_SCATTER_MINB 0  // >0: ask ptxas for that many resident CTAs per SM (register cap)
@@ -560,31 +566,42 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     const bool small = (P->flags & 256) || (!(P->flags & 128) && E * 8 <= static_cast<u64>(gridDim.x) * blockDim.x);
     if (ETWG_WS && W == 1 && !MMW && !small) {
         // Warp specialisation (measured: K1 alone is ~46 % of this kernel,
-        // the bucket scatter the rest, and in one warp they serialise). Warp
-        // w < kWsPairs is a producer: K1 for 32 consecutive parents, then
-        // (S, child mask) into its pair's double-buffered shared slot;
-        // warp w + kWsPairs is its consumer: takes the slot, releases it and
-        // emits the children (atomics + stores) while the producer already
-        // evaluates the next 32 parents. full/empty handshakes on mbarriers.
-        __shared__ u64 ws_S[kWsPairs][2][32], ws_M[kWsPairs][2][32], ws_base[kWsPairs][2];
-        __shared__ __align__(8) u64 ws_bar[kWsPairs][2][2];  // [pair][buffer][full, empty]
+        // the bucket scatter the rest, and in one warp they serialise). A
+        // producer warp runs K1 for 32 consecutive parents and puts
+        // (S, child mask) into the next slot of its ring; its consumer warps
+        // take slots in turn, release them and emit the children (atomics +
+        // stores) while the producer already evaluates the next 32 parents.
+        // full/empty handshakes on mbarriers.
+        __shared__ u64 ws_S[kWsProd][kWsRing][32], ws_M[kWsProd][kWsRing][32], ws_base[kWsProd][kWsRing];
+        __shared__ __align__(8) u64 ws_bar[kWsProd][kWsRing][2];  // [producer][slot][full, empty]
         const int warp = threadIdx.x >> 5;
-        const int pair = warp % kWsPairs;
-        if (threadIdx.x < kWsPairs * 4) mbar_init(&ws_bar[threadIdx.x >> 2][(threadIdx.x >> 1) & 1][threadIdx.x & 1], 1);
+        // producer p = warp < kWsProd; consumer warp kWsProd + p*kWsCpp + c
+        // takes producer p's tiles t with t % kWsCpp == c (slot t % kWsRing)
+        const int pair = warp < kWsProd ? warp : (warp - kWsProd) / kWsCpp;
+        const int role = warp < kWsProd ? 0 : (warp - kWsProd) % kWsCpp;
+        for (int i = threadIdx.x; i < kWsProd * kWsRing * 2; i += blockDim.x) mbar_init(&ws_bar[0][0][0] + i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         __syncthreads();
-        const u64 producers = static_cast<u64>(gridDim.x) * kWsPairs;
-        const u64 me = static_cast<u64>(blockIdx.x) * kWsPairs + pair;
-        if (warp < kWsPairs) {
+        const u64 producers = static_cast<u64>(gridDim.x) * kWsProd;
+        const u64 me = static_cast<u64>(blockIdx.x) * kWsProd + pair;
+        if (warp < kWsProd) {
+            // slot of tile t is free once the consumer of tile t - kWsRing released it
+            auto acquire = [&](unsigned t) {
+                if (t >= static_cast<unsigned>(kWsRing))
+                    mbar_wait(&ws_bar[pair][t % kWsRing][1], ((t / kWsRing) - 1) & 1u);
+            };
             for (unsigned it = 0;; ++it) {
-                const int b = it & 1;
-                if (it >= 2) mbar_wait(&ws_bar[pair][b][1], ((it >> 1) - 1) & 1u);  // consumer released it
+                const int b = it % kWsRing;
+                acquire(it);
                 const u64 base = (me + it * producers) * 32;
                 const bool done = base >= E || *reinterpret_cast<volatile unsigned*>(&C->abort) != 0;
-                if (done) {
-                    if (lane == 0) {
-                        ws_base[pair][b] = ~u64{0};
-                        mbar_arrive(&ws_bar[pair][b][0]);
+                if (done) {  // one end marker per consumer: tiles it .. it + kWsCpp - 1
+                    for (unsigned u = it; u < it + kWsCpp; ++u) {
+                        if (u != it) acquire(u);
+                        if (lane == 0) {
+                            ws_base[pair][u % kWsRing] = ~u64{0};
+                            mbar_arrive(&ws_bar[pair][u % kWsRing][0]);
+                        }
                     }
                     break;
                 }
@@ -606,9 +623,9 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
             }
         } else {
             const bool k1_only = (P->flags & 16384) && static_cast<int>(r) + 1 == P->rounds;  // diagnostics
-            for (unsigned it = 0;; ++it) {
-                const int b = it & 1;
-                mbar_wait(&ws_bar[pair][b][0], (it >> 1) & 1u);
+            for (unsigned it = role;; it += kWsCpp) {
+                const int b = it % kWsRing;
+                mbar_wait(&ws_bar[pair][b][0], (it / kWsRing) & 1u);
                 const u64 base = ws_base[pair][b];
                 if (base == ~u64{0}) break;
                 Set<W> S, M;
