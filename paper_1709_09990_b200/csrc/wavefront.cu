@@ -503,7 +503,12 @@ static_assert(kWsProd * (1 + kWsCpp) == kThreads / 32, "warp roles must fill the
 #define ETWG_SCATTER_BOUNDS __launch_bounds__(kThreads)
 #endif
 
-template <int W, bool MMW, bool BLOOM>
+// GT: 0 = this instantiation runs every round (both emission paths
+// compiled in); 1 = bucket rounds only, 2 = global-table rounds only (the
+// exact one-word instantiations: the host launches both, the plan picks,
+// the other returns at once — with both emission paths in one kernel ptxas
+// allocated 80 registers instead of 64, one resident CTA per SM less).
+template <int W, bool MMW, bool BLOOM, int GT = 0>
 __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P, Control* C,
                                                             Bufs B) {
     __shared__ Set<W> adj[64 * W];
@@ -514,6 +519,8 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
     const unsigned r = C->round;
     const u64 E = C->count[r & 1];
     const PartPlan pl = part_plan<W>(P, C, r, E, B.tab_cap);
+    if ((GT == 1 && pl.gtab) || (GT == 2 && !pl.gtab)) return;
+    const bool gt = GT == 2 ? true : GT == 1 ? false : pl.gtab != 0;  // compile-time where GT fixes it
     const u64 rec_need = pl.gtab ? 0 : (pl.np >> pl.lgp) * pl.cap * (W == 1 && pl.compact ? 1 : rec_words<W>());  // u64 words
     if (pl.np > B.cursor_cap || rec_need > B.rec_cap) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -635,14 +642,14 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 if (lane == 0) mbar_arrive(&ws_bar[pair][b][1]);
                 bool full = false;
                 if (k1_only) {
-                } else if (pl.gtab) {
+                } else if (gt) {
                     emit_lane_tab(B, pl, S.w[0], M.w[0], base + lane, full);
                 } else {
                     emit_lane<W>(B, pl, n, S, M, base + lane, full);
                 }
                 if (__any_sync(kFull, full) && lane == 0) {
                     C->need = 2 * pl.cap;
-                    C->abort = pl.gtab ? kGrowTable : kGrowRecs;
+                    C->abort = gt ? kGrowTable : kGrowRecs;
                 }
             }
         }
@@ -666,7 +673,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 Set<W> key = S;
                 key.add(v);
                 u64 low;
-                if (W == 1 && pl.gtab) {
+                if (W == 1 && gt) {
                     emit_lane_tab(B, pl, S.w[0], key.w[0] ^ S.w[0], p, full);
                     continue;
                 }
@@ -681,9 +688,10 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         }
         if (__any_sync(kFull, full) && lane == 0) {
             C->need = 2 * pl.cap;
-            C->abort = pl.gtab ? kGrowTable : kGrowRecs;
+            C->abort = gt ? kGrowTable : kGrowRecs;
         }
-    } else
+    } else if constexpr (!(ETWG_WS && W == 1 && !MMW)) {  // (dead for warp-specialised instantiations:
+                                                          // compiled out so its registers do not count)
     for (u64 base = ((blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5) * 32; base < E;
          base += nwarps * 32) {
         if (*reinterpret_cast<volatile unsigned*>(&C->abort)) break;  // warp-uniform read
@@ -703,7 +711,7 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         // last round evaluates its candidates but emits no records — times K1
         // without the bucket scatter
         if ((P->flags & 16384) && static_cast<int>(r) + 1 == P->rounds) continue;
-        if (W == 1 && pl.gtab) {
+        if (W == 1 && gt) {
             emit_lane_tab(B, pl, S.w[0], Me.w[0], idx, full);
         } else {
 #if ETWG_EMIT_FLAT == 0
@@ -748,8 +756,9 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         }
         if (__any_sync(kFull, full) && lane == 0) {
             C->need = 2 * pl.cap;
-            C->abort = pl.gtab ? kGrowTable : kGrowRecs;
+            C->abort = gt ? kGrowTable : kGrowRecs;
         }
+    }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -1701,6 +1710,7 @@ private:
     bool compact_possible_ = false;  // ETWG_COMPACT build or ETWG_DEBUG 8192 this decide
     unsigned passes_ = 1;            // hash-range passes per round (f4: records beyond HBM)
     bool gtab_ = false;              // this decide's small exact rounds may use the global table (W == 1)
+    int grid_bkt_ = 0, grid_tab_ = 0;  // k_exact_scatter<1, false, false, 1 / 2> grids
     bool part_bloom_ = false;  // Bloom rounds of this decide use scatter/part/append
 
     // Epochs tag look-back statuses (24 bits); on wrap-around the status
@@ -1800,10 +1810,14 @@ private:
             grid = prop.multiProcessorCount * std::max(1, blocks);
         };
         allow_exact(k_exact_scatter<1, false, false>, scatter_smem<1>(), grid_exact_[0]);
+        allow_exact(k_exact_scatter<1, false, false, 1>, scatter_smem<1>(), grid_bkt_);
+        allow_exact(k_exact_scatter<1, false, false, 2>, scatter_smem<1>(), grid_tab_);
         allow_exact(k_exact_scatter<2, false, false>, 0, grid_exact_[1]);
         if (const char* c = std::getenv("ETWG_SCATTER_CTAS")) {  // CTAs per SM (tuning sweeps)
             const int per = std::atoi(c);
             for (int w = 0; w < 2; ++w) grid_exact_[w] = std::min(grid_exact_[w], prop.multiProcessorCount * per);
+            grid_bkt_ = std::min(grid_bkt_, prop.multiProcessorCount * per);
+            grid_tab_ = std::min(grid_tab_, prop.multiProcessorCount * per);
         }
         allow_exact(k_exact_scatter<1, true, false>, 0, grid_exact_mmw_[0]);
         allow_exact(k_exact_scatter<2, true, false>, 0, grid_exact_mmw_[1]);
@@ -2087,7 +2101,12 @@ private:
             if (cfg.use_mmw)
                 timed_launch([&] { k_exact_scatter<W, true, BLOOM><<<grid_exact_mmw_[W - 1], kThreads, smem, stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.expand_ms, prof.t.expand_launches);
-            else
+            else if (W == 1 && !BLOOM && gtab_) {  // the plan picks one; the other returns at once
+                timed_launch([&] { k_exact_scatter<W, false, BLOOM, 1><<<grid_bkt_, kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.expand_ms, prof.t.expand_launches);
+                timed_launch([&] { k_exact_scatter<W, false, BLOOM, 2><<<grid_tab_, kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
+                             prof.t.expand_ms, prof.t.expand_launches);
+            } else
                 timed_launch([&] { k_exact_scatter<W, false, BLOOM><<<grid_exact_[W - 1], kThreads, scatter_smem<W>(), stream_>>>(d_params_, d_ctl_, b_); },
                              prof.t.expand_ms, prof.t.expand_launches);
             // the scatter's plan picks the round's dedup; the other kernels return at once

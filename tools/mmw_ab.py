@@ -1,0 +1,34 @@
+"""MMW timing probe (not a benchmark): solves with minor-min-width pruning in
+fresh processes, default scatter vs forced warp-per-parent candidate
+evaluation (ETWG_DEBUG 256), and checks the stats JSON is identical.
+Usage: python tools/mmw_ab.py [reps]"""
+import json, os, subprocess, sys
+
+CODE = r"""
+import json, sys, time
+sys.path.insert(0, '.')
+from paper_1709_09990_b200 import elimtw as E, generators as G
+out = {}
+for name, rows in (("queen6_6", G.queen_graph(6, 6)), ("myciel4", G.myciel(4)),
+                   ("g40", G.random_graph(1, 40, 0.3))):
+    g = E.Graph.from_rows(rows)
+    for dedup in ("exact", "bloom"):
+        o = E.Options(dedup=dedup, use_mmw=True, max_layer_states=1 << 31)
+        E.solve(g, o)
+        ts = []
+        for _ in range(int(sys.argv[1])):
+            t0 = time.perf_counter(); r = E.solve(g, o); ts.append(time.perf_counter() - t0)
+        out[name + "/" + dedup] = [min(ts), r.value, r.stats_json if dedup == "exact" else r.value]
+print(json.dumps(out))
+"""
+reps = sys.argv[1] if len(sys.argv) > 1 else "3"
+res = []
+for flags in ("0", "256"):
+    env = dict(os.environ, ETWG_DEBUG=flags)
+    p = subprocess.run([sys.executable, "-c", CODE, reps], env=env, capture_output=True, text=True, timeout=1800)
+    if p.returncode:
+        print("failed", p.stderr[-2000:]); sys.exit(1)
+    res.append(json.loads(p.stdout.strip().splitlines()[-1]))
+for k in res[0]:
+    a, b = res[0][k], res[1][k]
+    print(f"{k:18s} tw {a[1]}  default {a[0]*1e3:9.1f} ms  warp-per-parent {b[0]*1e3:9.1f} ms  identical {a[2] == b[2]}")
