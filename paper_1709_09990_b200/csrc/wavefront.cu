@@ -1621,6 +1621,7 @@ public:
     void release_buffers() {
         if (init_state_ != 1) return;
         check(cudaStreamSynchronize(stream_), "sync");
+        drop_graphs();
         for (int i = 0; i < 2; ++i) {
             cudaFree(b_.keys[i]);
             cudaFree(b_.hist[i]);
@@ -2131,6 +2132,74 @@ private:
                      prof.t.append_ms, prof.t.append_launches);
     }
 
+    // ---- CUDA graphs of round chunks ---------------------------------
+    // Every round kernel takes its sizes from device memory (Params,
+    // Control), so a chunk of `count` rounds is the same launch sequence
+    // for every chunk of that length: it is captured once per (W, mode,
+    // passes, count, buffer set) and replayed with one cudaGraphLaunch
+    // instead of 3-5 launches per round. A buffer reallocation changes the
+    // kernels' by-value Bufs, so the cached graph no longer matches and a
+    // new one is captured. Profiling runs (per-kernel events) and
+    // ETWG_GRAPHS=0 launch kernel by kernel.
+    struct RoundGraph {
+        int W, mode, count;
+        unsigned passes;
+        Bufs bufs;
+        cudaGraphExec_t exec;
+        uint64_t launches[4];  // kernel / expand / insert / append launches per replay
+    };
+    std::vector<RoundGraph> graphs_;
+    int use_graphs_ = -1;
+
+    void drop_graphs() {
+        for (RoundGraph& g : graphs_) cudaGraphExecDestroy(g.exec);
+        graphs_.clear();
+    }
+
+    template <int W>
+    void launch_rounds(const DpConfig& cfg, int count) {
+        if (use_graphs_ < 0) {
+            const char* e = std::getenv("ETWG_GRAPHS");
+            use_graphs_ = !(e && std::atoi(e) == 0);
+        }
+        if (prof.on || !use_graphs_) {
+            for (int i = 0; i < count; ++i) launch_round<W>(cfg);
+            return;
+        }
+        const int mode = (cfg.dedup == DedupMode::exact_set ? 1 : 0) | (cfg.use_mmw ? 2 : 0) | (part_bloom_ ? 4 : 0) |
+                         (gtab_ ? 8 : 0) | (compact_possible_ ? 16 : 0);
+        for (RoundGraph& g : graphs_) {
+            if (g.W == W && g.mode == mode && g.count == count && g.passes == passes_ &&
+                std::memcmp(&g.bufs, &b_, sizeof(Bufs)) == 0) {
+                check(cudaGraphLaunch(g.exec, stream_), "graph launch");
+                prof.t.kernel_launches += g.launches[0];
+                prof.t.expand_launches += g.launches[1];
+                prof.t.insert_launches += g.launches[2];
+                prof.t.append_launches += g.launches[3];
+                return;
+            }
+        }
+        const uint64_t before[4] = {prof.t.kernel_launches, prof.t.expand_launches, prof.t.insert_launches,
+                                    prof.t.append_launches};
+        cudaGraph_t graph = nullptr;
+        check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "graph capture");
+        for (int i = 0; i < count; ++i) launch_round<W>(cfg);
+        check(cudaStreamEndCapture(stream_, &graph), "graph capture end");
+        RoundGraph g{W, mode, count, passes_, b_, nullptr, {}};
+        check(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+        cudaGraphDestroy(graph);
+        g.launches[0] = prof.t.kernel_launches - before[0];
+        g.launches[1] = prof.t.expand_launches - before[1];
+        g.launches[2] = prof.t.insert_launches - before[2];
+        g.launches[3] = prof.t.append_launches - before[3];
+        if (graphs_.size() >= 48) {  // stale buffer sets / chunk lengths
+            cudaGraphExecDestroy(graphs_.front().exec);
+            graphs_.erase(graphs_.begin());
+        }
+        graphs_.push_back(g);
+        check(cudaGraphLaunch(g.exec, stream_), "graph launch");  // (the capture counted this replay's launches)
+    }
+
     void fetch_control() {
         copy(h_ctl_, d_ctl_, sizeof(Control), cudaMemcpyDeviceToHost, "control d2h");
         check(cudaStreamSynchronize(stream_), "sync");
@@ -2178,10 +2247,10 @@ private:
                 h_ctl_->epoch = epoch_;
                 copy(&d_ctl_->epoch, &h_ctl_->epoch, sizeof(unsigned), cudaMemcpyHostToDevice, "epoch reset");
             }
-            for (int r = start; r < end; ++r) {
-                if (W == 1) launch_round<1>(cfg);
-                else launch_round<2>(cfg);
-            }
+            if (W == 1)
+                launch_rounds<1>(cfg, end - start);
+            else
+                launch_rounds<2>(cfg, end - start);
             fetch_control();
             Control& c = *h_ctl_;
             if (c.abort != kOk) {
