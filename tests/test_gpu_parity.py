@@ -349,6 +349,16 @@ def test_global_table_equals_buckets(gpu):
     assert buckets == _run_with_env({"ETWG_DEBUG": "128"}, _TIGHT_CODE)
 
 
+def test_graph_replay_equals_launches(gpu):
+    """Round chunks replayed from captured CUDA graphs (default) give the
+    same layers, histories and counters as kernel-by-kernel launches
+    (ETWG_GRAPHS=0), including rounds that abort, grow a buffer (which
+    invalidates the cached graphs) and re-run."""
+    eager = _run_with_env({"ETWG_GRAPHS": "0"}, _TIGHT_CODE)
+    assert eager == _run_with_env({}, _TIGHT_CODE)
+    assert eager == _run_with_env({"ETWG_DEBUG": "1024"}, _TIGHT_CODE)
+
+
 def _run_with_debug(flags, code):
     """Runs `code` in a fresh interpreter with ETWG_DEBUG=flags (the engine
     reads it when a decide starts) and returns its JSON output."""
