@@ -367,8 +367,27 @@ __device__ __forceinline__ void record_store(const Bufs& B, const PartPlan& pl, 
 // per child, `full` set when a bucket is out of room.
 template <int W>
 __device__ __forceinline__ void emit_lane(const Bufs& B, const PartPlan& pl, int n, const Set<W>& S,
-                                          const Set<W>& M, u64 idx, bool& full) {
+                                          const Set<W>& M, u64 idx, bool& full, int diag = 0) {
     Set<W> rest = M;
+    if (diag) {
+        // diagnostics (ETWG_DEBUG 32768 / 65536, last round of a decide,
+        // results invalid): the same records without the cursor atomic's
+        // return — 1: slot from a per-lane sequence, no atomic; 2: the
+        // cursor bumped by a fire-and-forget RED, slot from the sequence
+        unsigned seq = static_cast<unsigned>(idx * 0x9E3779B1u);
+        while (rest.any()) {
+            const int v = pop_any(rest);
+            Set<W> key = S;
+            key.add(v);
+            u64 low;
+            const u64 part = record_part<W>(key, pl, n, low);
+            if (!pl.mine(part)) continue;
+            if (diag == 2) atomicAdd(cursor_at(B, part), 1u);  // result unused: RED
+            const unsigned slot = (seq += 0x61C88647u) % static_cast<unsigned>(pl.cap);
+            record_store<W>(B, pl, part, slot, key, low, idx, v);
+        }
+        return;
+    }
     constexpr int LU = ETWG_LANE_UNROLL;
     while (rest.any()) {
         Set<W> key[LU];
@@ -473,14 +492,32 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
                  : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-issuing the probe — the
+// plain loop spent ~5e9 of 26e9 warp instructions of the largest scatter
+// launch spinning here (ncu source page, r02aj)
+#ifndef ETWG_MBAR_SUSPEND_NS
+#define ETWG_MBAR_SUSPEND_NS 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
+    const unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+#if ETWG_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WSWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WSWAIT_%=;\n\t}" ::"r"(addr),
+        "r"(parity), "r"(ETWG_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WSWAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WSWAIT_%=;\n\t}" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+        "@!p bra WSWAIT_%=;\n\t}" ::"r"(addr),
         "r"(parity)
         : "memory");
+#endif
 }
 
 #ifndef ETWG_WS
@@ -645,7 +682,9 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 } else if (gt) {
                     emit_lane_tab(B, pl, S.w[0], M.w[0], base + lane, full);
                 } else {
-                    emit_lane<W>(B, pl, n, S, M, base + lane, full);
+                    const int diag = static_cast<int>(r) + 1 == P->rounds
+                                         ? ((P->flags & 32768) ? 1 : (P->flags & 65536) ? 2 : 0) : 0;
+                    emit_lane<W>(B, pl, n, S, M, base + lane, full, diag);
                 }
                 if (__any_sync(kFull, full) && lane == 0) {
                     C->need = 2 * pl.cap;
