@@ -408,7 +408,9 @@ __device__ __forceinline__ void emit_lane(const Bufs& B, const PartPlan& pl, int
         if (diag == 3) {  // diagnostics: a second returning atomic per record (to another cursor)
 #pragma unroll
             for (int u = 0; u < LU; ++u)
-                if (slot[u] != ~0u && atomicAdd(cursor_at(B, part[u] ^ 1), 0u) == 0xFFFFFFFFu) full = true;
+                if (slot[u] != ~0u &&
+                    atomicAdd(cursor_at(B, (part[u] + (pl.np >> 1) + 17) & (pl.np - 1)), 0u) == 0xFFFFFFFFu)
+                    full = true;  // (a cursor in another line)
         }
 #pragma unroll
         for (int u = 0; u < LU; ++u) {
