@@ -513,6 +513,9 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
 #ifndef ETWG_WS
 #define ETWG_WS 1  // warp-specialised scatter: K1 warps feed emission warps through shared memory
 #endif
+#ifndef ETWG_SWAP_DEDUP
+#define ETWG_SWAP_DEDUP 1  // sibling swap pre-dedup of each producer tile (k_exact_scatter, WS path)
+#endif
 #ifndef ETWG_WS_PROD
 #define ETWG_WS_PROD 4  // producer warps per CTA; the other warps consume, kWsCpp per producer
 #endif
@@ -653,8 +656,30 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                     M = warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned,
                                                                       mmw_keep);
                 }
+                const int offered_here = M.count();
+                if (ETWG_SWAP_DEDUP) {
+                    // Sibling swap pre-dedup: parents i < j of this tile with
+                    // S_i ^ S_j = {v, w} (v in S_j, w in S_i) share the child
+                    // S_i | S_j, offered by i through v and by j through w. When
+                    // both offer it, j's copy can never be the min-rank
+                    // emission (rank = idx*64 + vertex, idx_i < idx_j), so j
+                    // drops it before it becomes a record; the min-rank copy
+                    // of every key survives (the lowest lane never drops it).
+                    // Consecutive parents are often siblings (the layer is in
+                    // rank order), so this removes records at shuffle cost.
+                    const u64 Sm = S.w[0], M0 = M.w[0];
+                    u64 drop = 0;
+#pragma unroll 4
+                    for (int d = 1; d < 32; ++d) {
+                        const u64 So = __shfl_up_sync(kFull, Sm, d);
+                        const u64 Mo = __shfl_up_sync(kFull, M0, d);
+                        const u64 x = So ^ Sm;
+                        if (lane >= d && __popcll(x) == 2 && (Mo & x & Sm) != 0) drop |= x & So;
+                    }
+                    M.w[0] = M0 & ~drop;
+                }
                 if (pl.pass == 0) {
-                    offered += M.count();
+                    offered += offered_here;
                     winners += M.count();
                     if (valid) store_set<W>(B.cmask, idx, Set<W>::zero());
                 }
