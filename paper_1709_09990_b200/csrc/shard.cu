@@ -224,6 +224,21 @@ __global__ void __launch_bounds__(kRouteThreads) k_route(const Params* __restric
             adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep,
             (!TILE && !MMW && W == 1 && pl.shared_r) ? reinterpret_cast<Set<W>*>(smem_raw) : nullptr);
         offered += M.count();
+        if constexpr (ETWG_SWAP_DEDUP && W == 1 && !MMW && !TILE) {
+            // sibling swap pre-dedup (as in k_exact_scatter): of two parents
+            // of this warp whose sets differ by one swap, the higher-rank one
+            // does not route the child they share — fewer records cross NVLink
+            const u64 Sm = S.w[0], M0 = M.w[0];
+            u64 drop = 0;
+#pragma unroll 4
+            for (int d = 1; d < 32; ++d) {
+                const u64 So = __shfl_up_sync(kFull, Sm, d);
+                const u64 Mo = __shfl_up_sync(kFull, M0, d);
+                const u64 x = So ^ Sm;
+                if (lane >= d && __popcll(x) == 2 && (Mo & x & Sm) != 0) drop |= x & So;
+            }
+            M.w[0] = M0 & ~drop;
+        }
         if (pl.emit && valid) store_set<W>(B.cmask, idx, Set<W>::zero());
         if constexpr (TILE) {
             tile_set_clear<W, route_tile_slots<W>()>(ts);

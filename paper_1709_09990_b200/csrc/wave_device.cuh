@@ -27,6 +27,10 @@ constexpr unsigned kSeed2 = 0x5EEDBA5Eu;  // bloom.hpp:25
 
 using u64 = unsigned long long;
 
+#ifndef ETWG_SWAP_DEDUP
+#define ETWG_SWAP_DEDUP 1  // sibling swap pre-dedup of each warp's 32 parents (k_exact_scatter, k_route)
+#endif
+
 struct Params {
     int n, k, rounds, free_count;
     int hashes, bpe, any_pop, flags;  // flags: ETWG_DEBUG bits (tests only)

@@ -513,9 +513,6 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
 #ifndef ETWG_WS
 #define ETWG_WS 1  // warp-specialised scatter: K1 warps feed emission warps through shared memory
 #endif
-#ifndef ETWG_SWAP_DEDUP
-#define ETWG_SWAP_DEDUP 1  // sibling swap pre-dedup of each producer tile (k_exact_scatter, WS path)
-#endif
 #ifndef ETWG_WS_PROD
 #define ETWG_WS_PROD 4  // producer warps per CTA; the other warps consume, kWsCpp per producer
 #endif
