@@ -925,13 +925,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
     };
     u64 lp = blockIdx.x;
     if (lp < np && threadIdx.x == 0) issue(lp, count_of(lp), 0, 2);
+    // the table is cleared once; each bucket's mark pass empties the slots it used
+    for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+        keys[i] = 0;
+        ranks[i] = ~u64{0};
+    }
     for (; lp < np; lp += gridDim.x) {
         const u64 part = lp * passes + pass;
         const unsigned cnt = count_of(lp);
-        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
-            keys[i] = 0;
-            ranks[i] = ~u64{0};
-        }
         if (threadIdx.x == 0) s_full = 0;
         __syncthreads();
         const unsigned nch = (cnt + kTmaChunk - 1) / kTmaChunk;
@@ -971,10 +972,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_exact_part_tma(const Params*
         if (threadIdx.x == 0 && nxt < np) issue(nxt, count_of(nxt), 0, 2);
         for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
             const u64 rank = ranks[i];
-            if (rank == ~u64{0}) continue;
+            if (rank == ~u64{0}) continue;  // never claimed (a claimed slot always got a rank)
+            const u64 kw = keys[i];
+            keys[i] = 0;  // empty again for the next bucket
+            ranks[i] = ~u64{0};
             if constexpr (BLOOM) {
                 Set<1> key;
-                key.w[0] = keys[i];
+                key.w[0] = kw;
                 const u64 m = bloom_bits_for(round_cap(*P, C->count[r & 1]), P->bpe);
                 unsigned* bits = B.bloom[r & 1];
                 const unsigned h1 = murmur_key<1>(key, kSeed1);
@@ -1035,10 +1039,11 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
     const u64 np = C->rs[r].np / passes;  // this pass's buckets: part = lp * passes + pass
     const u64 cap = C->rs[r].pcap;
     u64 probed = 0;  // BLOOM: distinct keys sent through the filter (one atomic per thread at exit)
+    // the table is cleared once; each bucket's mark pass empties the slots it used
+    for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) keys[i] = 0;
+    for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) ranks[i] = ~u64{0};
     for (u64 lp = blockIdx.x; lp < np; lp += gridDim.x) {
         const u64 part = lp * passes + pass;
-        for (int i = threadIdx.x; i < SLOTS * W; i += blockDim.x) keys[i] = 0;
-        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) ranks[i] = ~u64{0};
         if (threadIdx.x == 0) s_full = 0;
         __syncthreads();
         const unsigned cnt = *cursor_at(B, part);
@@ -1094,11 +1099,15 @@ __global__ void __launch_bounds__(kPartThreads) k_exact_part(const Params* __res
         // mark each key's min-rank child in its parent's winner mask
         for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
             const u64 rank = ranks[i];
-            if (rank == ~u64{0}) continue;
-            if constexpr (BLOOM) {
-                Set<W> key;
+            if (rank == ~u64{0}) continue;  // never claimed
+            Set<W> key;
 #pragma unroll
-                for (int w = 0; w < W; ++w) key.w[w] = keys[W * i + w];
+            for (int w = 0; w < W; ++w) {
+                key.w[w] = keys[W * i + w];
+                keys[W * i + w] = 0;  // empty again for the next bucket
+            }
+            ranks[i] = ~u64{0};
+            if constexpr (BLOOM) {
                 const u64 m = bloom_bits_for(round_cap(*P, C->count[r & 1]), P->bpe);
                 unsigned* bits = B.bloom[r & 1];
                 const unsigned h1 = murmur_key<W>(key, kSeed1);
