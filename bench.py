@@ -300,7 +300,10 @@ def roofline(p):
             "wavefront_round_GBps": round_bytes / (total_ms / 1e3) / 1e9 if total_ms else None,
             "kernel_ms": {k: v[0] for k, v in classes.items()},
             "kernel_GBps": {k: (v[2] / (v[0] / 1e3) / 1e9 if v[0] else None) for k, v in classes.items()},
-            "children_offered": int(p["offered"]), "distinct_children": int(p["unique"])}
+            "children_offered": int(p["offered"]), "distinct_children": int(p["unique"]),
+            "child_records": int(p.get("records", 0)),
+            "algorithmic_bytes_note": "16 B per parent read + 16 B per winner-mask clear + 16 B per child "
+                                      "record written (children left after the sibling swap pre-dedup)"}
 
 
 def sharded_roofline(t, dev_ms, world):

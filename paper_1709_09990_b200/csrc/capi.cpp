@@ -430,7 +430,8 @@ int etwg_times(double* out, int len) {
                         static_cast<double>(t.offered),
                         static_cast<double>(t.unique),
                         static_cast<double>(t.bloom_probed),
-                        static_cast<double>(t.bloom_fp)};
+                        static_cast<double>(t.bloom_fp),
+                        t.records};
     int n = static_cast<int>(sizeof v / sizeof v[0]);
     if (len < n) n = len;
     for (int i = 0; i < n; ++i) out[i] = v[i];

@@ -132,6 +132,7 @@ struct KernelTimes {
     // insert / partition dedup, append
     double expand_bytes = 0, insert_bytes = 0, append_bytes = 0;
     uint64_t offered = 0, unique = 0;  // children offered to dedup / distinct children
+    double records = 0;                // exact rounds: child records written (after the swap pre-dedup)
     // partitioned Bloom rounds: distinct keys probed / rejected by the filter
     uint64_t bloom_probed = 0, bloom_fp = 0;
 };

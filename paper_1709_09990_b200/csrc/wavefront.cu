@@ -513,6 +513,9 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
 #ifndef ETWG_WS
 #define ETWG_WS 1  // warp-specialised scatter: K1 warps feed emission warps through shared memory
 #endif
+#ifndef ETWG_SWAP_CTA
+#define ETWG_SWAP_CTA 0  // 1: the swap test spans the CTA's kWsProd producer tiles (128 parents)
+#endif
 #ifndef ETWG_WS_PROD
 #define ETWG_WS_PROD 4  // producer warps per CTA; the other warps consume, kWsCpp per producer
 #endif
@@ -624,11 +627,25 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                 if (t >= static_cast<unsigned>(kWsRing))
                     mbar_wait(&ws_bar[pair][t % kWsRing][1], ((t / kWsRing) - 1) & 1u);
             };
+            // ETWG_SWAP_CTA: the CTA's producers hold kWsProd consecutive tiles
+            // per iteration (tiles blockIdx*kWsProd + p + it*producers); they
+            // share (S, M) through shared memory on a producer-only named
+            // barrier, so the swap test spans 32*kWsProd consecutive parents.
+            // Their stop decision must then be uniform: the group's first tile
+            // and an abort flag sampled by producer 0 before the barrier.
+            __shared__ u64 sw_S[ETWG_SWAP_CTA ? 2 : 1][kWsProd][32], sw_M[ETWG_SWAP_CTA ? 2 : 1][kWsProd][32];
+            __shared__ unsigned sw_stop[2];
+            if (ETWG_SWAP_CTA && threadIdx.x < 2) sw_stop[threadIdx.x] = 0;
+            if (ETWG_SWAP_CTA) asm volatile("bar.sync 1, %0;" ::"n"(kWsProd * 32) : "memory");
             for (unsigned it = 0;; ++it) {
                 const int b = it % kWsRing;
                 acquire(it);
                 const u64 base = (me + it * producers) * 32;
-                const bool done = base >= E || *reinterpret_cast<volatile unsigned*>(&C->abort) != 0;
+                const bool done =
+                    ETWG_SWAP_CTA
+                        ? (static_cast<u64>(blockIdx.x) * kWsProd + it * producers) * 32 >= E ||
+                              *reinterpret_cast<volatile unsigned*>(&sw_stop[it & 1]) != 0
+                        : base >= E || *reinterpret_cast<volatile unsigned*>(&C->abort) != 0;
                 if (done) {  // one end marker per consumer: tiles it .. it + kWsCpp - 1
                     for (unsigned u = it; u < it + kWsCpp; ++u) {
                         if (u != it) acquire(u);
@@ -666,6 +683,22 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                     // rank order), so this removes records at shuffle cost.
                     const u64 Sm = S.w[0], M0 = M.w[0];
                     u64 drop = 0;
+                    if (ETWG_SWAP_CTA) {
+                        sw_S[it & 1][pair][lane] = Sm;
+                        sw_M[it & 1][pair][lane] = M0;
+                        if (pair == 0 && lane == 0)
+                            sw_stop[(it + 1) & 1] = *reinterpret_cast<volatile unsigned*>(&C->abort) != 0;
+                        asm volatile("bar.sync 1, %0;" ::"n"(kWsProd * 32) : "memory");
+                        for (int q = 0; q < pair; ++q) {  // lower producers' tiles: all 32 parents rank lower
+#pragma unroll 4
+                            for (int d = 0; d < 32; ++d) {
+                                const u64 So = sw_S[it & 1][q][d];
+                                const u64 Mo = sw_M[it & 1][q][d];
+                                const u64 x = So ^ Sm;
+                                if (__popcll(x) == 2 && (Mo & x & Sm) != 0) drop |= x & So;
+                            }
+                        }
+                    }
 #pragma unroll 4
                     for (int d = 1; d < 32; ++d) {
                         const u64 So = __shfl_up_sync(kFull, Sm, d);
@@ -2487,10 +2520,19 @@ private:
                 // k_exact_part: record read, one winner-mask OR per distinct key
                 // (compact rounds: 8-byte records, plus the parent's set read
                 // back per distinct key)
-                const bool compact = s.round >= 0 && s.round < kMaxRounds && h_ctl_->rs[s.round].compact;
+                // Records are the children left after the producers' swap
+                // pre-dedup (RoundStats::winners), not every offered child.
+                const bool in_range = s.round >= 0 && s.round < kMaxRounds;
+                const bool compact = in_range && h_ctl_->rs[s.round].compact;
+                const double R = in_range && h_ctl_->rs[s.round].winners ? static_cast<double>(h_ctl_->rs[s.round].winners) : P;
                 const double rec = compact ? 8.0 : 8.0 * W + 8.0;
-                prof.t.expand_bytes += 2 * sb * E + rec * P;
-                prof.t.insert_bytes += rec * P + (compact ? 16.0 : 8.0) * U;
+                prof.t.expand_bytes += 2 * sb * E + rec * R;
+                prof.t.insert_bytes += rec * R + (compact ? 16.0 : 8.0) * U;
+                if (!compact) prof.t.records += R;
+                if (std::getenv("ETWG_TRACE") && in_range)
+                    std::fprintf(stderr, "[engine] round %d expanded %llu offered %llu records %llu distinct %llu\n", s.round,
+                                 static_cast<unsigned long long>(s.expanded), static_cast<unsigned long long>(P),
+                                 static_cast<unsigned long long>(R), static_cast<unsigned long long>(U));
             }
             // k_append: parent + history + mask read, state + history written
             prof.t.append_bytes += (sb + 4.0 + sb) * E + wb * U;

@@ -445,7 +445,7 @@ TIME_KEYS = ("decide_ms", "expand_ms", "insert_ms", "append_ms", "clear_ms", "fu
              "expand_launches", "insert_launches", "append_launches", "clear_launches",
              "fused_launches", "kernel_launches", "layer_bytes", "dedup_bytes", "expanded",
              "h2d_bytes", "d2h_bytes", "exchange_bytes", "reruns", "expand_bytes",
-             "insert_bytes", "append_bytes", "offered", "unique", "bloom_probed", "bloom_fp")
+             "insert_bytes", "append_bytes", "offered", "unique", "bloom_probed", "bloom_fp", "records")
 
 
 def times() -> dict:

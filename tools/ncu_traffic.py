@@ -16,9 +16,12 @@ for line in open(stats_path):
         rounds.append(tuple(int(x) for x in p))
 r, E, U, D = max(rounds, key=lambda t: t[2] + t[3])
 P = U + D
+# child records actually written (after the scatter's sibling swap
+# pre-dedup; ETWG_TRACE prints them per round): RECORDS=<n>, default P
+REC = int(__import__("os").environ.get("RECORDS", P))
 alg = {  # W = 1 (n <= 64) exact mode, bytes per launch
-    "k_exact_scatter": 16 * E + 16 * P,
-    "k_exact_part": 16 * P + 8 * U,
+    "k_exact_scatter": 16 * E + 16 * REC,
+    "k_exact_part": 16 * REC + 8 * U,
     "k_append": 20 * E + 12 * U,
     "k_route": 8 * E + 16 * P,
     "k_owner": 16 * P + 12 * U,
@@ -49,7 +52,7 @@ def metrics(rep):
             "sm_pct": val("sm__throughput.avg.pct_of_peak_sustained_elapsed")}
 
 
-res = {"round": {"index": r, "expanded": E, "emitted": U, "offered": P}}
+res = {"round": {"index": r, "expanded": E, "emitted": U, "offered": P, "records": REC}}
 for arg in sys.argv[3:]:
     name, rep = arg.split("=", 1)
     shards = 1
