@@ -513,6 +513,9 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
 #ifndef ETWG_WS
 #define ETWG_WS 1  // warp-specialised scatter: K1 warps feed emission warps through shared memory
 #endif
+#ifndef ETWG_SWAP_PAIR
+#define ETWG_SWAP_PAIR 1  // producer iterations take adjacent tile pairs: 64-parent swap window (0: one tile)
+#endif
 #ifndef ETWG_SWAP_CTA
 #define ETWG_SWAP_CTA 0  // 1: the swap test spans the CTA's kWsProd producer tiles (128 parents)
 #endif
@@ -525,12 +528,7 @@ constexpr int kWsRing = 2 * kWsCpp;                           // shared slots pe
 static_assert(kWsProd * (1 + kWsCpp) == kThreads / 32, "warp roles must fill the CTA");
 
 #ifndef ETWG_SCATTER_MINB
-#define ETWG_SCATTER_MINB 0  // >0: ask ptxas for that many resident CTAs per SM (register cap)
-#endif
-#if ETWG_SCATTER_MINB > 0
-#define ETWG_SCATTER_BOUNDS __launch_bounds__(kThreads, ETWG_SCATTER_MINB)
-#else
-#define ETWG_SCATTER_BOUNDS __launch_bounds__(kThreads)
+#define ETWG_SCATTER_MINB 0  // >0: resident CTAs per SM asked of ptxas for the scatter instantiations other than the bucket-only exact one
 #endif
 
 // GT: 0 = this instantiation runs every round (both emission paths
@@ -538,8 +536,12 @@ static_assert(kWsProd * (1 + kWsCpp) == kThreads / 32, "warp roles must fill the
 // exact one-word instantiations: the host launches both, the plan picks,
 // the other returns at once — with both emission paths in one kernel ptxas
 // allocated 80 registers instead of 64, one resident CTA per SM less).
+// The bucket-only exact instantiation is held to 64 registers (4 CTAs per
+// SM): with the tile-pair swap window ptxas otherwise takes 79 (measured
+// 0.911 vs 0.921 s per G48 solve with the cap).
 template <int W, bool MMW, bool BLOOM, int GT = 0>
-__global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P, Control* C,
+__global__ void __launch_bounds__(kThreads, (W == 1 && !MMW && !BLOOM && GT == 1) ? 4 : (ETWG_SCATTER_MINB > 0 ? ETWG_SCATTER_MINB : 2))
+k_exact_scatter(const Params* __restrict__ P, Control* C,
                                                             Bufs B) {
     __shared__ Set<W> adj[64 * W];
     __shared__ unsigned mmw_keep[MMW ? kThreads : 1][2 * W];
@@ -637,10 +639,14 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
             __shared__ unsigned sw_stop[2];
             if (ETWG_SWAP_CTA && threadIdx.x < 2) sw_stop[threadIdx.x] = 0;
             if (ETWG_SWAP_CTA) asm volatile("bar.sync 1, %0;" ::"n"(kWsProd * 32) : "memory");
+            // ETWG_SWAP_PAIR: iterations 2q, 2q+1 take two adjacent tiles, so
+            // the odd one also tests against the even one's 32 parents
+            u64 prevS = 0, prevM = 0;
             for (unsigned it = 0;; ++it) {
                 const int b = it % kWsRing;
                 acquire(it);
-                const u64 base = (me + it * producers) * 32;
+                const u64 base = ETWG_SWAP_PAIR ? ((me + (it >> 1) * producers) * 2 + (it & 1)) * 32
+                                                : (me + it * producers) * 32;
                 const bool done =
                     ETWG_SWAP_CTA
                         ? (static_cast<u64>(blockIdx.x) * kWsProd + it * producers) * 32 >= E ||
@@ -705,6 +711,20 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
                         const u64 Mo = __shfl_up_sync(kFull, M0, d);
                         const u64 x = So ^ Sm;
                         if (lane >= d && __popcll(x) == 2 && (Mo & x & Sm) != 0) drop |= x & So;
+                    }
+                    if (ETWG_SWAP_PAIR) {
+                        if (it & 1) {  // the even tile's 32 parents all rank lower
+#pragma unroll 4
+                            for (int d = 0; d < 32; ++d) {
+                                const u64 So = __shfl_sync(kFull, prevS, d);
+                                const u64 Mo = __shfl_sync(kFull, prevM, d);
+                                const u64 x = So ^ Sm;
+                                if (__popcll(x) == 2 && (Mo & x & Sm) != 0) drop |= x & So;
+                            }
+                        } else {
+                            prevS = Sm;
+                            prevM = M0;
+                        }
                     }
                     M.w[0] = M0 & ~drop;
                 }
@@ -794,6 +814,18 @@ __global__ void ETWG_SCATTER_BOUNDS k_exact_scatter(const Params* __restrict__ P
         const Set<W> M =
             warp_candidates<W, MMW, ETWG_SCATTER_COMPACT>(adj, P->n, P->k, S, valid, forbidden, pruned, mmw_keep);
         Set<W> Me = M;  // the children this lane emits
+        if constexpr (ETWG_SWAP_DEDUP && W == 1) {  // sibling swap pre-dedup over the warp's 32 parents
+            const u64 Sm = S.w[0], M0 = M.w[0];
+            u64 drop = 0;
+#pragma unroll 4
+            for (int d = 1; d < 32; ++d) {
+                const u64 So = __shfl_up_sync(kFull, Sm, d);
+                const u64 Mo = __shfl_up_sync(kFull, M0, d);
+                const u64 x = So ^ Sm;
+                if (lane >= d && __popcll(x) == 2 && (Mo & x & Sm) != 0) drop |= x & So;
+            }
+            Me.w[0] = M0 & ~drop;
+        }
         if (pl.pass == 0) {  // counters and mask clear once per round, not per pass
             offered += M.count();
             winners += Me.count();
