@@ -540,7 +540,7 @@ static_assert(kWsProd * (1 + kWsCpp) == kThreads / 32, "warp roles must fill the
 // SM): with the tile-pair swap window ptxas otherwise takes 79 (measured
 // 0.911 vs 0.921 s per G48 solve with the cap).
 template <int W, bool MMW, bool BLOOM, int GT = 0>
-__global__ void __launch_bounds__(kThreads, (W == 1 && !MMW && !BLOOM && GT == 1) ? 4 : (ETWG_SCATTER_MINB > 0 ? ETWG_SCATTER_MINB : 2))
+__global__ void __launch_bounds__(kThreads, (W == 1 && !MMW && !BLOOM && GT != 0) ? 4 : (ETWG_SCATTER_MINB > 0 ? ETWG_SCATTER_MINB : 2))
 k_exact_scatter(const Params* __restrict__ P, Control* C,
                                                             Bufs B) {
     __shared__ Set<W> adj[64 * W];
